@@ -1,0 +1,159 @@
+/*
+ * us_api.h — C ABI of the B200-native UniSparse hot path (sm_100a).
+ *
+ * Drop-in boundary for the reference operator API (namespace unisparse,
+ * /root/reference/proj/include/unisparse/):
+ *
+ *   reference (C++, by value, exceptions)              this ABI (C, device pointers, status)
+ *   -------------------------------------------------  -----------------------------------------
+ *   compress(in, cfg)            compression.hpp:89    us_compress
+ *   select_blocks(UniSparse, in, cfg) pipeline.hpp:19  us_select
+ *   build_block_mask(scores,P,c_h,H) selection.hpp:41  us_build_block_mask
+ *   block_sparse_attention(in, mask) attention.hpp:27  us_sparse_attention
+ *   unisparse_attn(in, cfg)      pipeline.hpp:16       us_unisparse_attention
+ *   dense_attention(in, causal)  attention.hpp:21      us_dense_attention (causal only)
+ *   validate_inputs(in, cfg)     types.hpp:106         us_validate
+ *   selection_flops(...)         metrics.hpp:31        us_selection_flops
+ *   CompressionConfig / AttentionInputs types.hpp:54-72  us_params
+ *
+ * Conventions
+ *   * Tensors are device pointers, head-major (the reference HeadStack order,
+ *     tensor_io.hpp:9-11) with a leading batch dim:
+ *       Q, O      bf16 [B][H][L][d_k]
+ *       K, V      bf16 [B][H_kv][L][d_k]   (GQA: head h reads KV head h/(H/H_kv);
+ *                                          H_kv == H is the reference layout)
+ *       lse       f32  [B][H][L]           natural log, reference AttentionOutput::lse
+ *   * Selection planes: one plane per compressed head (H/c_h planes); head h
+ *     uses plane h / c_h (the broadcast of selection.cpp:80-84).
+ *       mask_bits u32  [B][planes][N][W], W = ceil(N/32); bit (j%32) of word
+ *                 j/32 in row i set <=> key block j is attended by query block i.
+ *   * No allocation inside timed calls: the caller passes a workspace of at
+ *     least us_workspace_bytes(params) bytes (device memory).
+ *   * `stream` is a cudaStream_t (void* keeps CUDA headers out of this file).
+ *     Calls are asynchronous unless US_FLAG_SYNC_CHECK is set in params.flags,
+ *     in which case the call synchronizes the stream and reports data errors
+ *     (negative/NaN proxy scores, malformed masks) the way the reference throws.
+ *   * No C++ exceptions cross this boundary. Errors return a us_status and set
+ *     a thread-local message (us_last_error) carrying the reference's text,
+ *     e.g. "select_blocks: L=1000 not divisible by S=64".
+ *   * Reentrant: no global mutable state besides per-thread error text and
+ *     per-device one-time init (std::call_once).
+ */
+#ifndef US_API_H
+#define US_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum us_status {
+  US_OK = 0,
+  US_ERR_INVALID_ARGUMENT = 1, /* shapes / config: reference std::invalid_argument */
+  US_ERR_UNSUPPORTED = 2,      /* valid for the reference, not on this GPU path (e.g. d_k=96) */
+  US_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
+  US_ERR_INVALID_MASK = 4,     /* non-causal bit or empty row (attention.cpp:106-108,127-129) */
+  US_ERR_NONFINITE = 5,        /* negative/NaN proxy scores (selection.cpp:14-15) */
+  US_ERR_WORKSPACE = 6         /* workspace missing or too small */
+} us_status;
+
+/* PoolStrategy (types.hpp:34) — the GPU path implements Mean. */
+enum { US_POOL_MEAN = 0, US_POOL_MAX = 1, US_POOL_STOCHASTIC = 2 };
+/* CausalMode (types.hpp:36-42) */
+enum { US_POST_SOFTMAX_BLOCK_CAUSAL = 0, US_PRE_SOFTMAX_COMPRESSED_CAUSAL = 1 };
+/* selection rule: reference Top-P (selection.cpp:11-48), or top-k = first k of the same order */
+enum { US_SELECT_TOP_P = 0, US_SELECT_TOP_K = 1 };
+/* ProxyTag (types.hpp:45) for us_selection_flops */
+enum { US_PROXY_UNISPARSE = 0, US_PROXY_ANTIDIAGONAL = 1, US_PROXY_LAST_BLOCK = 2 };
+/* params.flags */
+enum { US_FLAG_SYNC_CHECK = 1 };
+
+/* CompressionConfig (types.hpp:54-62) + AttentionInputs dims (types.hpp:66-72)
+ * + the GQA / batch / top-k extensions the north star adds. */
+typedef struct us_params {
+  int32_t B;           /* batch */
+  int32_t H;           /* query heads */
+  int32_t H_kv;        /* key/value heads (H % H_kv == 0) */
+  int32_t L;           /* sequence length (L % S == 0) */
+  int32_t d_k;         /* head dim (GPU path: 64 or 128) */
+  int32_t S;           /* block size (GPU path: 64) */
+  int32_t c_q, c_k, c_h;
+  int32_t strategy;    /* US_POOL_* */
+  int32_t causal_mode; /* US_POST_SOFTMAX_BLOCK_CAUSAL (reference default) or pre */
+  int32_t select_mode; /* US_SELECT_TOP_P / US_SELECT_TOP_K */
+  double P;            /* Top-P mass threshold in (0, 1], kept in double (types.hpp:59) */
+  int32_t top_k;       /* k for US_SELECT_TOP_K */
+  int32_t flags;       /* US_FLAG_* */
+  uint64_t seed;       /* stochastic pooling seed (unused by Mean) */
+} us_params;
+
+/* Selection outputs (device pointers; every field except mask_bits may be NULL).
+ * The reference SparsityReport (metrics.hpp:77-83) is derived from counts. */
+typedef struct us_selection {
+  uint32_t* mask_bits; /* [B][planes][N][W] */
+  int32_t* counts;     /* [B][planes][N] selected blocks per row */
+  double* coverage;    /* [B][planes][N] covered score fraction (BlockMask::coverage) */
+  float* scores;       /* [B][planes][N][N] proxy block scores, j <= i written */
+  int16_t* indices;    /* [B][planes][N][N] ascending selected block ids, counts[] valid */
+} us_selection;
+
+const char* us_version(void);
+const char* us_last_error(void);
+
+/* validate_inputs (types.cpp:97-123) plus GPU-path constraints. Returns the
+ * number of violations; msg receives them joined by "; ". */
+int us_validate(const us_params* p, char* msg, size_t cap);
+
+/* Device workspace needed by any call below for these params. */
+size_t us_workspace_bytes(const us_params* p);
+
+/* compress (compression.cpp:5-25), Mean pooling: Qc f32 [B][H/c_h][L/c_q][d_k],
+ * Kc f32 [B][H/c_h][L/c_k][d_k] (K expanded to H heads first, as the reference). */
+us_status us_compress(const us_params* p, const void* Q, const void* K, float* Qc, float* Kc,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* select_blocks (pipeline.cpp:5-17): compress -> proxy -> Top-P/top-k selection. */
+us_status us_select(const us_params* p, const void* Q, const void* K, const us_selection* out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* build_block_mask (selection.cpp:60-88) on given f32 block scores
+ * [B][planes][N][N] (only j <= i read). */
+us_status us_build_block_mask(const us_params* p, const float* scores, const us_selection* out,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* block_sparse_attention (attention.cpp:89-137). heads_per_plane maps head h to
+ * mask plane h / heads_per_plane (1 = one plane per head, as the reference). */
+us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, const void* V,
+                              const uint32_t* mask_bits, int32_t heads_per_plane, void* O,
+                              float* lse, void* workspace, size_t workspace_bytes, void* stream);
+
+/* unisparse_attn (pipeline.cpp:19-24). sel may be NULL; if given, its non-NULL
+ * fields receive the selection (mask_bits is then also used by attention). */
+us_status us_unisparse_attention(const us_params* p, const void* Q, const void* K, const void* V,
+                                 void* O, float* lse, const us_selection* sel, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/* Causal dense attention through the same kernel with every causal block
+ * selected (the P = 1 path; reference criterion 1). */
+us_status us_dense_attention(const us_params* p, const void* Q, const void* K, const void* V,
+                             void* O, float* lse, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+/* Reads and clears the device-side data-error word of a workspace
+ * (synchronizes the stream). */
+us_status us_check_device_errors(const us_params* p, void* workspace, void* stream);
+
+/* selection_flops (metrics.cpp:44-81): out6 = compression, compressed_qk,
+ * softmax_aggregation, top_p, sparse_attention (0), dense_attention. */
+us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, uint64_t* out6);
+
+/* Number of kernel launches the last successful call on this thread issued. */
+int32_t us_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* US_API_H */

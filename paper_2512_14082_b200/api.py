@@ -1,0 +1,378 @@
+"""Python mirror of the reference operator API over the C ABI (include/us_api.h).
+
+Names, arguments and error behaviour follow /root/reference/proj/include/unisparse/:
+
+    compress(Q, K, cfg)                    -> (Qc, Kc)            compression.hpp:89
+    select_blocks(Q, K, cfg)               -> SparsityReport      pipeline.hpp:19
+    build_block_mask(scores, cfg)          -> Selection           selection.hpp:41
+    block_sparse_attention(Q, K, V, mask)  -> (O, lse)            attention.hpp:27
+    unisparse_attn(Q, K, V, cfg)           -> UniSparseResult     pipeline.hpp:16
+    dense_attention(Q, K, V)               -> (O, lse)            attention.hpp:21
+
+Tensors are torch CUDA tensors (torch is only the device-memory/stream
+plumbing here): Q bf16 [B,H,L,d], K/V bf16 [B,H_kv,L,d] (3-D inputs are
+treated as B = 1). Shape/config violations raise ValueError carrying the
+reference's message ("select_blocks: L=1000 not divisible by S=64"), exactly
+where the reference throws std::invalid_argument. There is no CPU fallback:
+without the CUDA library every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+import os
+import threading
+from typing import Optional
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_build", "libunisparse_b200.so")
+
+US_OK, US_ERR_INVALID_ARGUMENT, US_ERR_UNSUPPORTED, US_ERR_CUDA, US_ERR_INVALID_MASK, \
+    US_ERR_NONFINITE, US_ERR_WORKSPACE = range(7)
+POOL_MEAN, POOL_MAX, POOL_STOCHASTIC = 0, 1, 2
+POST_SOFTMAX_BLOCK_CAUSAL, PRE_SOFTMAX_COMPRESSED_CAUSAL = 0, 1
+SELECT_TOP_P, SELECT_TOP_K = 0, 1
+PROXY_UNISPARSE, PROXY_ANTIDIAGONAL, PROXY_LAST_BLOCK = 0, 1, 2
+FLAG_SYNC_CHECK = 1
+
+
+class UnsupportedError(ValueError):
+    """Valid for the reference, outside what the GPU path implements."""
+
+
+class InvalidMaskError(ValueError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class UsParams(C.Structure):
+    _fields_ = [("B", C.c_int32), ("H", C.c_int32), ("H_kv", C.c_int32), ("L", C.c_int32),
+                ("d_k", C.c_int32), ("S", C.c_int32), ("c_q", C.c_int32), ("c_k", C.c_int32),
+                ("c_h", C.c_int32), ("strategy", C.c_int32), ("causal_mode", C.c_int32),
+                ("select_mode", C.c_int32), ("P", C.c_double), ("top_k", C.c_int32),
+                ("flags", C.c_int32), ("seed", C.c_uint64)]
+
+
+class UsSelection(C.Structure):
+    _fields_ = [("mask_bits", C.c_void_p), ("counts", C.c_void_p), ("coverage", C.c_void_p),
+                ("scores", C.c_void_p), ("indices", C.c_void_p)]
+
+
+@dataclasses.dataclass
+class CompressionConfig:
+    """types.hpp:54-62, plus the north-star extensions (top-k selection)."""
+    c_q: int = 8
+    c_k: int = 8
+    c_h: int = 1
+    strategy: int = POOL_MEAN
+    P: float = 0.95
+    causal_mode: int = POST_SOFTMAX_BLOCK_CAUSAL
+    seed: int = 0
+    select_mode: int = SELECT_TOP_P
+    top_k: int = 0
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise CudaError(f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+            _lib = C.CDLL(LIB_PATH)
+            L = _lib
+            L.us_version.restype = C.c_char_p
+            L.us_last_error.restype = C.c_char_p
+            L.us_validate.argtypes = [C.POINTER(UsParams), C.c_char_p, C.c_size_t]
+            L.us_workspace_bytes.restype = C.c_size_t
+            L.us_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+            vp = C.c_void_p
+            L.us_compress.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.c_size_t, vp]
+            L.us_select.argtypes = [C.POINTER(UsParams), vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
+            L.us_build_block_mask.argtypes = [C.POINTER(UsParams), vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
+            L.us_sparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_size_t, vp]
+            L.us_unisparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
+            L.us_dense_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+            L.us_check_device_errors.argtypes = [C.POINTER(UsParams), vp, vp]
+            L.us_selection_flops.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp]
+            L.us_selftest_umma.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]
+            L.us_last_launch_count.restype = C.c_int32
+        return _lib
+
+
+def _raise(status: int, default: str = ""):
+    if status == US_OK:
+        return
+    msg = lib().us_last_error().decode() or default
+    if status == US_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == US_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status in (US_ERR_INVALID_MASK, US_ERR_NONFINITE):
+        raise InvalidMaskError(msg) if status == US_ERR_INVALID_MASK else ValueError(msg)
+    raise CudaError(f"status {status}: {msg}")
+
+
+def _stream(t: Optional[torch.Tensor] = None):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def make_params(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64,
+                sync_check: bool = False) -> UsParams:
+    B, H, L, d = _bhld(Q)
+    H_kv = _bhld(K)[1]
+    return UsParams(B, H, H_kv, L, d, S, cfg.c_q, cfg.c_k, cfg.c_h, cfg.strategy, cfg.causal_mode,
+                    cfg.select_mode, float(cfg.P), cfg.top_k, FLAG_SYNC_CHECK if sync_check else 0,
+                    cfg.seed)
+
+
+def _bhld(x: torch.Tensor):
+    if x.dim() == 3:
+        return (1, *x.shape)
+    if x.dim() != 4:
+        raise ValueError(f"expected [B,H,L,d] or [H,L,d] tensor, got shape {tuple(x.shape)}")
+    return tuple(x.shape)
+
+
+def _check_inputs(*ts: torch.Tensor):
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("inputs must be CUDA tensors (the GPU path has no CPU fallback)")
+        if t.dtype != torch.bfloat16:
+            raise ValueError(f"inputs must be bfloat16, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError("inputs must be contiguous")
+
+
+# ------------------------------------------------------------------ workspace cache
+_ws_cache: dict = {}
+
+
+def workspace(p: UsParams) -> torch.Tensor:
+    need = lib().us_workspace_bytes(C.byref(p))
+    dev = torch.cuda.current_device()
+    cur = _ws_cache.get(dev)
+    if cur is None or cur.numel() < need:
+        cur = torch.empty(max(need, 256), dtype=torch.uint8, device=f"cuda:{dev}")
+        _ws_cache[dev] = cur
+    return cur
+
+
+def validate(p: UsParams) -> str:
+    buf = C.create_string_buffer(4096)
+    lib().us_validate(C.byref(p), buf, 4096)
+    return buf.value.decode()
+
+
+# ------------------------------------------------------------------ results
+@dataclasses.dataclass
+class Selection:
+    mask_bits: torch.Tensor         # int32 view of u32 words [B, planes, N, W]
+    counts: torch.Tensor            # [B, planes, N]
+    coverage: torch.Tensor          # [B, planes, N] float64
+    scores: Optional[torch.Tensor]  # [B, planes, N, N] float32
+    indices: Optional[torch.Tensor] # [B, planes, N, N] int16
+    c_h: int
+    N: int
+
+    def dense_mask(self, H: Optional[int] = None) -> torch.Tensor:
+        """Boolean [B, H, N, N] mask (planes broadcast to heads, selection.cpp:80-84)."""
+        words = self.mask_bits.to(torch.int64) & 0xFFFFFFFF
+        bits = ((words.unsqueeze(-1) >> torch.arange(32, device=words.device)) & 1).bool()
+        m = bits.flatten(-2)[..., : self.N]
+        return m.repeat_interleave(self.c_h, dim=1)
+
+
+@dataclasses.dataclass
+class SparsityReport:
+    """metrics.hpp:77-83 — rho per head, selected per head, FLOP breakdown, mask."""
+    rho: list
+    rho_mean: float
+    selected: list
+    flops: dict
+    mask: Selection
+
+
+@dataclasses.dataclass
+class UniSparseResult:
+    O: torch.Tensor
+    lse: torch.Tensor
+    report: SparsityReport
+
+
+FLOP_KEYS = ("compression", "compressed_qk", "softmax_aggregation", "top_p", "sparse_attention",
+             "dense_attention")
+
+
+def selection_flops(p: UsParams, proxy: int = PROXY_UNISPARSE, stride: int = 8) -> dict:
+    out = (C.c_uint64 * 6)()
+    _raise(lib().us_selection_flops(C.byref(p), proxy, stride, C.cast(out, C.c_void_p)))
+    return {k: int(v) for k, v in zip(FLOP_KEYS, out)}
+
+
+def _alloc_selection(p: UsParams, with_scores: bool, with_indices: bool) -> Selection:
+    dev = torch.cuda.current_device()
+    planes, N = p.H // p.c_h, p.L // p.S
+    W = (N + 31) // 32
+    return Selection(
+        mask_bits=torch.empty((p.B, planes, N, W), dtype=torch.int32, device=dev),
+        counts=torch.empty((p.B, planes, N), dtype=torch.int32, device=dev),
+        coverage=torch.empty((p.B, planes, N), dtype=torch.float64, device=dev),
+        scores=torch.zeros((p.B, planes, N, N), dtype=torch.float32, device=dev) if with_scores else None,
+        indices=torch.empty((p.B, planes, N, N), dtype=torch.int16, device=dev) if with_indices else None,
+        c_h=p.c_h, N=N)
+
+
+def _sel_struct(s: Selection) -> UsSelection:
+    return UsSelection(s.mask_bits.data_ptr(), s.counts.data_ptr(), s.coverage.data_ptr(),
+                       s.scores.data_ptr() if s.scores is not None else None,
+                       s.indices.data_ptr() if s.indices is not None else None)
+
+
+def make_report(p: UsParams, sel: Selection) -> SparsityReport:
+    """make_sparsity_report (metrics.cpp:226-237) from per-row counts."""
+    N = p.L // p.S
+    per_plane = sel.counts.to(torch.int64).sum(-1)                 # [B, planes]
+    per_head = per_plane.repeat_interleave(p.c_h, dim=1)           # [B, H]
+    selected = per_head.sum(0).tolist() if p.B > 1 else per_head[0].tolist()
+    causal = N * (N + 1) / 2.0
+    rho = [1.0 - s / (causal * p.B) for s in selected]
+    flops = selection_flops(p)
+    flops["sparse_attention"] = int(sum(selected)) * 4 * p.S * p.S * p.d_k
+    return SparsityReport(rho=rho, rho_mean=sum(rho) / len(rho), selected=selected, flops=flops, mask=sel)
+
+
+# ------------------------------------------------------------------ operators
+def compress(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64):
+    """compress (compression.cpp:5-25): f32 Qc [B,H/c_h,L/c_q,d], Kc [B,H/c_h,L/c_k,d]."""
+    _check_inputs(Q, K)
+    p = make_params(Q, K, cfg, S)
+    B, H, L, d = _bhld(Q)
+    Hc = max(H // max(cfg.c_h, 1), 1)
+    Qc = torch.empty((B, Hc, L // max(cfg.c_q, 1), d), dtype=torch.float32, device=Q.device)
+    Kc = torch.empty((B, Hc, L // max(cfg.c_k, 1), d), dtype=torch.float32, device=Q.device)
+    _raise(lib().us_compress(C.byref(p), _ptr(Q), _ptr(K), _ptr(Qc), _ptr(Kc), None, 0, _stream()))
+    return Qc, Kc
+
+
+def select_blocks(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64,
+                  with_scores: bool = False, with_indices: bool = False,
+                  sync_check: bool = True) -> SparsityReport:
+    """select_blocks(UniSparse, ...) (pipeline.cpp:5-17)."""
+    _check_inputs(Q, K)
+    p = make_params(Q, K, cfg, S, sync_check)
+    ws = workspace(p)
+    sel = _alloc_selection(p, with_scores, with_indices)
+    ss = _sel_struct(sel)
+    _raise(lib().us_select(C.byref(p), _ptr(Q), _ptr(K), C.byref(ss), _ptr(ws), ws.numel(), _stream()))
+    return make_report(p, sel)
+
+
+def build_block_mask(scores: torch.Tensor, cfg: CompressionConfig, H: Optional[int] = None,
+                     S: int = 64, with_indices: bool = False) -> Selection:
+    """build_block_mask (selection.cpp:60-88) on f32 block scores [B, planes, N, N]."""
+    if scores.dim() == 3:
+        scores = scores.unsqueeze(0)
+    if scores.dtype != torch.float32 or not scores.is_cuda:
+        raise ValueError("scores must be a float32 CUDA tensor")
+    scores = scores.contiguous()
+    B, planes, N, _ = scores.shape
+    H = planes * cfg.c_h if H is None else H
+    p = UsParams(B, H, H, N * S, 64, S, cfg.c_q, cfg.c_k, cfg.c_h, cfg.strategy, cfg.causal_mode,
+                 cfg.select_mode, float(cfg.P), cfg.top_k, FLAG_SYNC_CHECK, cfg.seed)
+    ws = workspace(p)
+    sel = _alloc_selection(p, False, with_indices)
+    ss = _sel_struct(sel)
+    _raise(lib().us_build_block_mask(C.byref(p), _ptr(scores), C.byref(ss), _ptr(ws), ws.numel(), _stream()))
+    return sel
+
+
+def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: int = 1, S: int = 64,
+                           validate_mask: bool = True, with_lse: bool = True):
+    """block_sparse_attention (attention.cpp:89-137). mask_bits: int32 [B, planes, N, W]."""
+    _check_inputs(Q, K, V)
+    p = make_params(Q, K, CompressionConfig(c_q=1, c_k=1, c_h=1), S, validate_mask)
+    O = torch.empty_like(Q)
+    B, H, L, _ = _bhld(Q)
+    lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
+    ws = workspace(p) if validate_mask else None
+    _raise(lib().us_sparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(mask_bits.contiguous()),
+                                     heads_per_plane, _ptr(O), _ptr(lse), _ptr(ws),
+                                     ws.numel() if ws is not None else 0, _stream()))
+    return O, lse
+
+
+def unisparse_attn(Q, K, V, cfg: CompressionConfig, S: int = 64, with_scores: bool = False,
+                   with_indices: bool = False, sync_check: bool = True) -> UniSparseResult:
+    """unisparse_attn (pipeline.cpp:19-24)."""
+    _check_inputs(Q, K, V)
+    p = make_params(Q, K, cfg, S, sync_check)
+    ws = workspace(p)
+    sel = _alloc_selection(p, with_scores, with_indices)
+    ss = _sel_struct(sel)
+    O = torch.empty_like(Q)
+    B, H, L, _ = _bhld(Q)
+    lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device)
+    _raise(lib().us_unisparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse),
+                                        C.byref(ss), _ptr(ws), ws.numel(), _stream()))
+    return UniSparseResult(O=O, lse=lse, report=make_report(p, sel))
+
+
+def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True):
+    """Causal dense attention via the same kernel with every causal block selected."""
+    _check_inputs(Q, K, V)
+    p = make_params(Q, K, CompressionConfig(c_q=1, c_k=1, c_h=1), S)
+    O = torch.empty_like(Q)
+    B, H, L, _ = _bhld(Q)
+    lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
+    _raise(lib().us_dense_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse), None, 0,
+                                    _stream()))
+    return O, lse
+
+
+class Engine:
+    """Allocation-free repeated calls (bench / serving): params, workspace and
+    selection buffers are created once; run() only launches kernels."""
+
+    def __init__(self, Q, K, V, cfg: CompressionConfig, S: int = 64):
+        _check_inputs(Q, K, V)
+        self.p = make_params(Q, K, cfg, S)
+        self.ws = workspace(self.p)
+        self.sel = _alloc_selection(self.p, False, False)
+        self.ss = _sel_struct(self.sel)
+        self.O = torch.empty_like(Q)
+        B, H, L, _ = _bhld(Q)
+        self.lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device)
+        self.Q, self.K, self.V = Q, K, V
+
+    def run(self, dense: bool = False):
+        if dense:
+            _raise(lib().us_dense_attention(C.byref(self.p), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
+                                            _ptr(self.O), _ptr(self.lse), None, 0, _stream()))
+        else:
+            _raise(lib().us_unisparse_attention(C.byref(self.p), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
+                                                _ptr(self.O), _ptr(self.lse), C.byref(self.ss),
+                                                _ptr(self.ws), self.ws.numel(), _stream()))
+        return self.O
+
+    def launches(self) -> int:
+        return int(lib().us_last_launch_count())
+
+
+def selftest_umma(mode: int, N: int, bf16: bool, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    D = torch.empty((128, N), dtype=torch.float32, device=A.device)
+    _raise(lib().us_selftest_umma(mode, N, int(bf16), _ptr(A), _ptr(B), _ptr(D), _stream()))
+    return D

@@ -1,0 +1,514 @@
+// api.cu — the C ABI (include/us_api.h): validation with the reference's
+// messages, workspace layout, TMA descriptors and kernel orchestration.
+//
+// Pipeline of us_unisparse_attention (pipeline.cpp:19-24), all on one stream:
+//   compress Q, compress K (f32 + per-plane absmax)        compress.cu
+//   split Q, split K (fp16 hi/lo, per-plane 2^e)           compress.cu
+//   proxy pass 1 (row lse), pass 2 (block scores)          proxy.cu   (tcgen05)
+//   select (+ exact fallback for uncertified rows)         select.cu
+//   block-sparse attention                                 attention.cu (tcgen05)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "host_util.hpp"
+#include "kernels.cuh"
+
+namespace us {
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+int& launch_counter() { return g_launches; }
+
+namespace {
+
+constexpr int kGpuBlock = 64;
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+struct Checked {
+  std::vector<std::string> errors;       // reference validate_inputs violations
+  std::vector<std::string> unsupported;  // valid for the reference, not on this GPU path
+};
+
+// validate_inputs (types.cpp:97-123) — same order and text — then GQA/batch
+// extensions, then GPU-path constraints.
+Checked check(const us_params& p, bool need_compression) {
+  Checked c;
+  auto& e = c.errors;
+  if (p.H <= 0) e.push_back("H must be positive");
+  if (p.L <= 0) e.push_back("L must be positive");
+  if (p.d_k <= 0) e.push_back("d_k must be positive");
+  if (p.S <= 0) e.push_back("S must be positive");
+  if (p.L > 0 && p.S > 0 && p.L % p.S != 0)
+    e.push_back("L=" + std::to_string(p.L) + " not divisible by S=" + std::to_string(p.S));
+  if (p.c_q <= 0) e.push_back("c_q must be positive");
+  if (p.c_k <= 0) e.push_back("c_k must be positive");
+  if (p.c_h <= 0) e.push_back("c_h must be positive");
+  if (p.S > 0 && p.c_q > 0 && p.S % p.c_q != 0)
+    e.push_back("S=" + std::to_string(p.S) + " not divisible by c_q=" + std::to_string(p.c_q));
+  if (p.S > 0 && p.c_k > 0 && p.S % p.c_k != 0)
+    e.push_back("S=" + std::to_string(p.S) + " not divisible by c_k=" + std::to_string(p.c_k));
+  if (p.H > 0 && p.c_h > 0 && p.H % p.c_h != 0)
+    e.push_back("H=" + std::to_string(p.H) + " not divisible by c_h=" + std::to_string(p.c_h));
+  if (!(p.P > 0.0) || p.P > 1.0) e.push_back("P must lie in (0, 1]");
+  if (p.H_kv <= 0) e.push_back("H_kv must be positive");
+  if (p.H > 0 && p.H_kv > 0 && p.H % p.H_kv != 0)
+    e.push_back("H=" + std::to_string(p.H) + " not divisible by H_kv=" + std::to_string(p.H_kv));
+  if (p.B <= 0) e.push_back("B must be positive");
+  if (p.select_mode != US_SELECT_TOP_P && p.select_mode != US_SELECT_TOP_K)
+    e.push_back("unknown select_mode");
+  if (p.select_mode == US_SELECT_TOP_K && p.top_k < 1) e.push_back("top_k must be positive");
+  if (p.causal_mode != US_POST_SOFTMAX_BLOCK_CAUSAL && p.causal_mode != US_PRE_SOFTMAX_COMPRESSED_CAUSAL)
+    e.push_back("unknown causal_mode");
+  if (!e.empty()) return c;
+  auto& u = c.unsupported;
+  if (p.d_k != 64 && p.d_k != 128)
+    u.push_back("d_k=" + std::to_string(p.d_k) + " unsupported on the GPU path (64 or 128)");
+  if (p.S != kGpuBlock) u.push_back("S=" + std::to_string(p.S) + " unsupported on the GPU path (64)");
+  if (p.L / std::max(p.S, 1) > 4096) u.push_back("N=L/S above 4096 unsupported on the GPU path");
+  if ((long long)p.B * p.H * p.L >= (1ll << 31)) u.push_back("B*H*L must stay below 2^31 rows");
+  if (need_compression) {
+    if (p.strategy != US_POOL_MEAN) u.push_back("only mean pooling is implemented on the GPU path");
+    if (!is_pow2(p.S / p.c_q) || !is_pow2(p.S / p.c_k))
+      u.push_back("S/c_q and S/c_k must be powers of two on the GPU path");
+  }
+  return c;
+}
+
+std::string joined(const std::vector<std::string>& v) {
+  std::string s;
+  for (size_t i = 0; i < v.size(); ++i) s += (i ? "; " : "") + v[i];
+  return s;
+}
+
+us_status gate(const us_params* p, const char* who, bool need_compression) {
+  g_launches = 0;
+  if (!p) {
+    set_error(std::string(who) + ": null params");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  Checked c = check(*p, need_compression);
+  if (!c.errors.empty()) {
+    set_error(std::string(who) + ": " + joined(c.errors));
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if (!c.unsupported.empty()) {
+    set_error(std::string(who) + ": " + joined(c.unsupported));
+    return US_ERR_UNSUPPORTED;
+  }
+  return US_OK;
+}
+
+// ---------------------------------------------------------------- geometry
+struct Geo {
+  int B, H, H_kv, G, L, D, S, N, W, Hc, Lq, Lk, rq, rk;
+  bool kv_dedup;
+  int kv_planes, kv_mul, kv_div;
+  explicit Geo(const us_params& p) {
+    B = p.B;
+    H = p.H;
+    H_kv = p.H_kv;
+    G = H / H_kv;
+    L = p.L;
+    D = p.d_k;
+    S = p.S;
+    N = L / S;
+    W = (N + 31) / 32;
+    Hc = H / p.c_h;
+    Lq = L / p.c_q;
+    Lk = L / p.c_k;
+    rq = S / p.c_q;
+    rk = S / p.c_k;
+    kv_dedup = (G % p.c_h) == 0;
+    kv_planes = kv_dedup ? H_kv : Hc;
+    kv_mul = kv_dedup ? p.c_h : 1;
+    kv_div = kv_dedup ? G : 1;
+  }
+};
+
+struct Ws {
+  size_t err, first_bad, fb_count, absmax_q, absmax_k, exp_q, exp_k, fb_rows, qc, kc, qh, ql, kh,
+      kl, lse2, scores, mask, total;
+  size_t header_bytes;  // [0, header_bytes) is cleared before each selection
+};
+
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+Ws layout(const us_params& p) {
+  Geo g(p);
+  Ws w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = al(o + bytes);
+    return at;
+  };
+  const size_t qplanes = size_t(g.B) * g.Hc, kplanes = size_t(g.B) * g.kv_planes;
+  w.err = take(4);
+  w.first_bad = take(4);
+  w.fb_count = take(4);
+  w.absmax_q = take(4 * qplanes);
+  w.absmax_k = take(4 * kplanes);
+  w.header_bytes = o;
+  w.exp_q = take(4 * qplanes);
+  w.exp_k = take(4 * kplanes);
+  const size_t rows = qplanes * g.N;
+  w.fb_rows = take(4 * rows);
+  // +128 rows of padding keep every TMA box inside the allocation
+  const size_t qrows = qplanes * g.Lq + 128, krows = kplanes * g.Lk + 128;
+  w.qc = take(4 * qrows * g.D);
+  w.kc = take(4 * krows * g.D);
+  w.qh = take(2 * qrows * g.D);
+  w.ql = take(2 * qrows * g.D);
+  w.kh = take(2 * krows * g.D);
+  w.kl = take(2 * krows * g.D);
+  w.lse2 = take(4 * qplanes * g.Lq);
+  w.scores = take(4 * rows * g.N);
+  w.mask = take(4 * rows * g.W);
+  w.total = o;
+  return w;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + off);
+}
+
+us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, size_t* need_out = nullptr) {
+  const size_t need = layout(p).total;
+  if (need_out) *need_out = need;
+  if (!ws || bytes < need) {
+    set_error(std::string(who) + ": workspace of " + std::to_string(need) + " bytes required");
+    return US_ERR_WORKSPACE;
+  }
+  return US_OK;
+}
+
+// compress + split + proxy (pass 1, 2) into ws.scores.
+us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, cudaStream_t st) {
+  Geo g(p);
+  Ws w = layout(p);
+  US_CUDA_TRY(cudaMemsetAsync(ws, 0, w.header_bytes, st), "workspace clear");
+  CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p.c_q, g.Hc, p.c_h, 1,
+                  at<float>(ws, w.qc), at<uint32_t>(ws, w.absmax_q)};
+  us_status s = launch_compress(cq, st);
+  if (s != US_OK) return s;
+  CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p.c_k, g.kv_planes,
+                  g.kv_dedup ? 1 : p.c_h, g.kv_dedup ? 1 : g.G, at<float>(ws, w.kc),
+                  at<uint32_t>(ws, w.absmax_k)};
+  if ((s = launch_compress(ck, st)) != US_OK) return s;
+  SplitArgs sq{at<float>(ws, w.qc), g.B * g.Hc, g.Lq, g.D, at<uint32_t>(ws, w.absmax_q),
+               at<int>(ws, w.exp_q), at<__half>(ws, w.qh), at<__half>(ws, w.ql)};
+  if ((s = launch_split(sq, st)) != US_OK) return s;
+  SplitArgs sk{at<float>(ws, w.kc), g.B * g.kv_planes, g.Lk, g.D, at<uint32_t>(ws, w.absmax_k),
+               at<int>(ws, w.exp_k), at<__half>(ws, w.kh), at<__half>(ws, w.kl)};
+  if ((s = launch_split(sk, st)) != US_OK) return s;
+
+  const uint64_t qrows = uint64_t(g.B) * g.Hc * g.Lq + 128, krows = uint64_t(g.B) * g.kv_planes * g.Lk + 128;
+  CUtensorMap tQh, tQl, tKh, tKl;
+  if ((s = make_tmap_2d_16b(&tQh, at<void>(ws, w.qh), qrows, g.D, 128, 64, false)) != US_OK) return s;
+  if ((s = make_tmap_2d_16b(&tQl, at<void>(ws, w.ql), qrows, g.D, 128, 64, false)) != US_OK) return s;
+  if ((s = make_tmap_2d_16b(&tKh, at<void>(ws, w.kh), krows, g.D, 128, 64, false)) != US_OK) return s;
+  if ((s = make_tmap_2d_16b(&tKl, at<void>(ws, w.kl), krows, g.D, 128, 64, false)) != US_OK) return s;
+  ProxyArgs pa{};
+  pa.B = g.B;
+  pa.Hc = g.Hc;
+  pa.Lq = g.Lq;
+  pa.Lk = g.Lk;
+  pa.N = g.N;
+  pa.D = g.D;
+  pa.rq = g.rq;
+  pa.rk = g.rk;
+  pa.c_q = p.c_q;
+  pa.c_k = p.c_k;
+  pa.causal_mode = p.causal_mode;
+  pa.kv_planes = g.kv_planes;
+  pa.kv_mul = g.kv_mul;
+  pa.kv_div = g.kv_div;
+  pa.exp_q = at<int>(ws, w.exp_q);
+  pa.exp_k = at<int>(ws, w.exp_k);
+  pa.lse2 = at<float>(ws, w.lse2);
+  pa.scores = at<float>(ws, w.scores);
+  pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  if ((s = launch_proxy(pa, tQh, tQl, tKh, tKl, 1, st)) != US_OK) return s;
+  return launch_proxy(pa, tQh, tQl, tKh, tKl, 2, st);
+}
+
+us_status run_select_rows(const us_params& p, const float* scores, int planes, uint32_t* mask,
+                          const us_selection* sel, void* ws, cudaStream_t st) {
+  Geo g(p);
+  Ws w = layout(p);
+  SelectArgs sa{};
+  sa.scores = scores;
+  sa.rows = g.B * planes * g.N;
+  sa.N = g.N;
+  sa.W = g.W;
+  sa.select_mode = p.select_mode;
+  sa.P = p.P;
+  sa.top_k = p.top_k;
+  sa.mask_bits = mask;
+  sa.counts = sel ? sel->counts : nullptr;
+  sa.coverage = sel ? sel->coverage : nullptr;
+  sa.indices = sel ? sel->indices : nullptr;
+  sa.err = at<uint32_t>(ws, w.err);
+  sa.fb_count = at<int32_t>(ws, w.fb_count);
+  sa.fb_rows = at<int32_t>(ws, w.fb_rows);
+  return launch_select(sa, st);
+}
+
+us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
+                        const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st) {
+  Geo g(p);
+  CUtensorMap tQ, tK, tV;
+  us_status s;
+  if ((s = make_tmap_2d_16b(&tQ, Q, uint64_t(g.B) * g.H * g.L, g.D, 64, 64, true)) != US_OK) return s;
+  if ((s = make_tmap_2d_16b(&tK, K, uint64_t(g.B) * g.H_kv * g.L, g.D, 64, 64, true)) != US_OK) return s;
+  if ((s = make_tmap_2d_16b(&tV, V, uint64_t(g.B) * g.H_kv * g.L, g.D, 64, 64, true)) != US_OK) return s;
+  AttnArgs a{};
+  a.B = g.B;
+  a.H = g.H;
+  a.H_kv = g.H_kv;
+  a.L = g.L;
+  a.N = g.N;
+  a.W = g.W;
+  a.D = g.D;
+  a.pair_heads = (g.G % 2 == 0) ? 1 : 0;
+  a.heads_per_plane = hpp;
+  a.planes = g.H / hpp;
+  a.mask = mask;
+  a.O = static_cast<__nv_bfloat16*>(O);
+  a.lse = lse;
+  a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  return launch_attention(a, tQ, tK, tV, st);
+}
+
+us_status sync_check(const us_params& p, void* ws, cudaStream_t st, const char* who) {
+  Ws w = layout(p);
+  US_CUDA_TRY(cudaStreamSynchronize(st), "stream synchronize");
+  uint32_t hdr[2] = {0, 0};
+  US_CUDA_TRY(cudaMemcpy(&hdr[0], at<void>(ws, w.err), 4, cudaMemcpyDeviceToHost), "error word read");
+  US_CUDA_TRY(cudaMemcpy(&hdr[1], at<void>(ws, w.first_bad), 4, cudaMemcpyDeviceToHost), "error row read");
+  US_CUDA_TRY(cudaMemset(at<void>(ws, w.err), 0, 4), "error word clear");
+  const uint32_t err = hdr[0];
+  if (err & 1u) {
+    set_error("top_p_row: scores must be nonnegative");
+    return US_ERR_NONFINITE;
+  }
+  if (err & 4u) {
+    set_error(std::string(who) + ": mask selects a non-causal block");
+    return US_ERR_INVALID_MASK;
+  }
+  if (err & 8u) {
+    Geo g(p);
+    set_error(std::string(who) + ": query block " + std::to_string(int(hdr[1]) % g.N) +
+              " has no selected key block");
+    return US_ERR_INVALID_MASK;
+  }
+  return US_OK;
+}
+
+}  // namespace
+}  // namespace us
+
+using namespace us;
+
+extern "C" {
+
+const char* us_version(void) { return "unisparse-b200 0.1 (sm_100a)"; }
+const char* us_last_error(void) { return g_err.c_str(); }
+int32_t us_last_launch_count(void) { return g_launches; }
+
+int us_validate(const us_params* p, char* msg, size_t cap) {
+  if (!p) return 1;
+  Checked c = check(*p, true);
+  std::vector<std::string> all = c.errors;
+  all.insert(all.end(), c.unsupported.begin(), c.unsupported.end());
+  if (msg && cap) std::snprintf(msg, cap, "%s", joined(all).c_str());
+  return int(all.size());
+}
+
+size_t us_workspace_bytes(const us_params* p) {
+  if (!p || !check(*p, false).errors.empty()) return 0;
+  return layout(*p).total;
+}
+
+us_status us_compress(const us_params* p, const void* Q, const void* K, float* Qc, float* Kc,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  us_status s = gate(p, "compress", true);
+  if (s != US_OK) return s;
+  Geo g(*p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // reference layout: H/c_h planes for both Q and K (K expanded to H heads first)
+  CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p->c_q, g.Hc, p->c_h, 1, Qc, nullptr};
+  if ((s = launch_compress(cq, st)) != US_OK) return s;
+  CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p->c_k, g.Hc, p->c_h, g.G, Kc, nullptr};
+  if ((s = launch_compress(ck, st)) != US_OK) return s;
+  if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "compress");
+  return US_OK;
+}
+
+us_status us_select(const us_params* p, const void* Q, const void* K, const us_selection* out,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  us_status s = gate(p, "select_blocks", true);
+  if (s != US_OK) return s;
+  if ((s = need_ws(*p, workspace, workspace_bytes, "select_blocks")) != US_OK) return s;
+  Geo g(*p);
+  Ws w = layout(*p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((s = run_proxy(*p, Q, K, workspace, st)) != US_OK) return s;
+  if (out && out->scores)
+    US_CUDA_TRY(cudaMemcpyAsync(out->scores, at<float>(workspace, w.scores),
+                                size_t(4) * g.B * g.Hc * g.N * g.N, cudaMemcpyDeviceToDevice, st),
+                "scores copy");
+  uint32_t* mask = (out && out->mask_bits) ? out->mask_bits : at<uint32_t>(workspace, w.mask);
+  if ((s = run_select_rows(*p, at<float>(workspace, w.scores), g.Hc, mask, out, workspace, st)) != US_OK)
+    return s;
+  if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "select_blocks");
+  return US_OK;
+}
+
+us_status us_build_block_mask(const us_params* p, const float* scores, const us_selection* out,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  us_status s = gate(p, "build_block_mask", false);
+  if (s != US_OK) return s;
+  if ((s = need_ws(*p, workspace, workspace_bytes, "build_block_mask")) != US_OK) return s;
+  if (!out || !out->mask_bits) {
+    set_error("build_block_mask: out->mask_bits is required");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  Geo g(*p);
+  Ws w = layout(*p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
+  if ((s = run_select_rows(*p, scores, g.Hc, out->mask_bits, out, workspace, st)) != US_OK) return s;
+  if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "build_block_mask");
+  return US_OK;
+}
+
+us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, const void* V,
+                              const uint32_t* mask_bits, int32_t heads_per_plane, void* O,
+                              float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+  us_status s = gate(p, "block_sparse_attention", false);
+  if (s != US_OK) return s;
+  if (heads_per_plane <= 0 || p->H % heads_per_plane != 0) {
+    set_error("block_sparse_attention: heads_per_plane must divide H");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if (!mask_bits) {
+    set_error("block_sparse_attention: mask_bits is required");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  Geo g(*p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p->flags & US_FLAG_SYNC_CHECK) {
+    if ((s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK) return s;
+    Ws w = layout(*p);
+    US_CUDA_TRY(cudaMemsetAsync(workspace, 0, 4, st), "workspace clear");
+    US_CUDA_TRY(cudaMemsetAsync(at<uint8_t>(workspace, w.first_bad), 0x7F, 4, st), "workspace clear");
+    if ((s = launch_mask_check(mask_bits, g.B * (g.H / heads_per_plane) * g.N, g.N, g.W,
+                               at<uint32_t>(workspace, w.err), at<int32_t>(workspace, w.first_bad), st)) != US_OK)
+      return s;
+    if ((s = sync_check(*p, workspace, st, "block_sparse_attention")) != US_OK) return s;
+  }
+  if ((s = run_attention(*p, Q, K, V, mask_bits, heads_per_plane, O, lse, st)) != US_OK) return s;
+  if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "block_sparse_attention");
+  return US_OK;
+}
+
+us_status us_unisparse_attention(const us_params* p, const void* Q, const void* K, const void* V,
+                                 void* O, float* lse, const us_selection* sel, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  us_status s = gate(p, "unisparse_attn", true);
+  if (s != US_OK) return s;
+  if ((s = need_ws(*p, workspace, workspace_bytes, "unisparse_attn")) != US_OK) return s;
+  Geo g(*p);
+  Ws w = layout(*p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((s = run_proxy(*p, Q, K, workspace, st)) != US_OK) return s;
+  if (sel && sel->scores)
+    US_CUDA_TRY(cudaMemcpyAsync(sel->scores, at<float>(workspace, w.scores),
+                                size_t(4) * g.B * g.Hc * g.N * g.N, cudaMemcpyDeviceToDevice, st),
+                "scores copy");
+  uint32_t* mask = (sel && sel->mask_bits) ? sel->mask_bits : at<uint32_t>(workspace, w.mask);
+  if ((s = run_select_rows(*p, at<float>(workspace, w.scores), g.Hc, mask, sel, workspace, st)) != US_OK)
+    return s;
+  const int launches = g_launches;
+  if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st)) != US_OK) return s;
+  (void)launches;
+  if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "unisparse_attn");
+  return US_OK;
+}
+
+us_status us_dense_attention(const us_params* p, const void* Q, const void* K, const void* V,
+                             void* O, float* lse, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  us_status s = gate(p, "dense_attention", false);
+  if (s != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((s = run_attention(*p, Q, K, V, nullptr, 1, O, lse, st)) != US_OK) return s;
+  if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "dense_attention");
+  return US_OK;
+}
+
+us_status us_check_device_errors(const us_params* p, void* workspace, void* stream) {
+  if (!p || !workspace) {
+    set_error("us_check_device_errors: null argument");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  return sync_check(*p, workspace, static_cast<cudaStream_t>(stream), "unisparse_attn");
+}
+
+us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, uint64_t* f) {
+  // metrics.cpp:44-81 (exact u64)
+  if (!p || !f) return US_ERR_INVALID_ARGUMENT;
+  const uint64_t L = uint64_t(p->L), H = uint64_t(p->H), d = uint64_t(p->d_k), S = uint64_t(p->S);
+  if (p->L <= 0 || p->H <= 0 || p->d_k <= 0 || p->S <= 0 || L % S != 0) {
+    set_error("selection_flops: bad dimensions");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  const uint64_t N = L / S;
+  uint64_t lg = 0;
+  while ((uint64_t(1) << lg) < N) ++lg;
+  for (int t = 0; t < 6; ++t) f[t] = 0;
+  f[5] = 4 * L * L * H * d;
+  if (proxy == US_PROXY_UNISPARSE) {
+    if (p->c_q <= 0 || p->c_k <= 0 || p->c_h <= 0 || S % uint64_t(p->c_q) || S % uint64_t(p->c_k) ||
+        H % uint64_t(p->c_h)) {
+      set_error("selection_flops: bad compression factors");
+      return US_ERR_INVALID_ARGUMENT;
+    }
+    const uint64_t cq = p->c_q, ck = p->c_k, ch = p->c_h;
+    f[0] = 2 * L * H * d + (ch > 1 ? 2 * (L / cq + L / ck) * H * d : 0);
+    f[1] = 2 * (L / cq) * (L / ck) * (H / ch) * d;
+    f[2] = 4 * (L / cq) * (L / ck) * (H / ch);
+    f[3] = (H / ch) * N * N * lg;
+  } else if (proxy == US_PROXY_ANTIDIAGONAL) {
+    if (stride <= 0 || S % uint64_t(stride)) {
+      set_error("selection_flops: stride must divide S");
+      return US_ERR_INVALID_ARGUMENT;
+    }
+    f[1] = 2 * L * (L / stride) * H * d;
+    f[2] = 2 * L * (L / stride) * H;
+    f[3] = H * N * N * lg;
+  } else {
+    f[1] = 2 * S * L * H * d;
+    f[2] = 2 * S * L * H;
+    f[3] = H * N * N * lg;
+  }
+  return US_OK;
+}
+
+}  // extern "C"

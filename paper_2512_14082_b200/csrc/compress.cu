@@ -1,0 +1,173 @@
+// compress.cu — multi-granularity compression.
+//
+// Reference: pool_sequence Mean (compression.hpp:26-28) then pool_heads
+// (compression.hpp:61-76), driven by compress (compression.cpp:5-25).
+//
+// Bit-exactness: each window is summed in fp64 in row order, divided by c in
+// fp64 and rounded once to f32; head groups are then summed in fp64 in member
+// order, divided by c_h and rounded again — the reference's two roundings. For
+// bf16 (and f32) inputs the fp64 window sum is exact, so the result does not
+// depend on summation order and matches the reference/oracle bit for bit.
+//
+// Memory plan: one thread owns 8 consecutive d-elements of one output row and
+// streams c rows of 16 B (8 x bf16) each: a warp covers 2 rows x 256 B, fully
+// coalesced 128-bit loads, several loads in flight per thread. HBM-bound:
+// bytes = planes_in * L * d * 2 (read) + planes_out * (L/c) * d * 4 (write).
+#include "host_util.hpp"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace us {
+namespace {
+
+__device__ __forceinline__ void bf16x8_to_f64_add(const uint4 v, double (&acc)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    acc[2 * t] += double(__uint_as_float(w[t] << 16));
+    acc[2 * t + 1] += double(__uint_as_float(w[t] & 0xFFFF0000u));
+  }
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// inv: exact reciprocal when the divisor is a power of two (then x*inv == x/div
+// bit for bit), else 0 and a true fp64 division is used.
+__device__ __forceinline__ double divide(double x, double div, double inv) {
+  return inv != 0.0 ? x * inv : x / div;
+}
+
+__global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
+  const int chunks = a.d / 8;
+  const int Lc = a.L / a.c;
+  const long long total = (long long)a.B * a.planes * Lc * chunks;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = tid < total;
+  float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int plane_id = 0;
+  if (active) {
+    const int ch = int(tid % chunks);
+    long long r = tid / chunks;
+    const int t = int(r % Lc);
+    r /= Lc;
+    const int p = int(r % a.planes);
+    const int b = int(r / a.planes);
+    plane_id = b * a.planes + p;
+    double hacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int g = 0; g < a.members; ++g) {
+      const int hs = (p * a.members + g) / a.div;
+      const uint4* src = reinterpret_cast<const uint4*>(
+          a.src + (((long long)b * a.H_src + hs) * a.L + (long long)t * a.c) * a.d + ch * 8);
+      const int stride = a.d / 8;  // uint4 per row
+      double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int rr = 0;
+      for (; rr + 8 <= a.c; rr += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(src + (rr + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bf16x8_to_f64_add(v[u], acc);
+      }
+      for (; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
+      if (a.members == 1) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) res[e] = __double2float_rn(divide(acc[e], double(a.c), inv_c));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          hacc[e] += double(__double2float_rn(divide(acc[e], double(a.c), inv_c)));
+      }
+    }
+    if (a.members > 1) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) res[e] = __double2float_rn(divide(hacc[e], double(a.members), inv_m));
+    }
+    float4* dst = reinterpret_cast<float4*>(a.out + (((long long)plane_id) * Lc + t) * a.d + ch * 8);
+    dst[0] = make_float4(res[0], res[1], res[2], res[3]);
+    dst[1] = make_float4(res[4], res[5], res[6], res[7]);
+  }
+  if (a.absmax) {
+    float m = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(res[e]));
+    // NaN sorts above every finite value as unsigned bits; keep it visible.
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (res[e] != res[e]) m = __uint_as_float(0x7FC00000u);
+    const unsigned full = __activemask();
+    const int leader_plane = __shfl_sync(full, plane_id, 0);
+    const bool uniform = __all_sync(full, !active || plane_id == leader_plane);
+    uint32_t bits = __float_as_uint(m);
+    if (uniform) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(full, bits, o));
+      if ((threadIdx.x & 31) == 0 && bits) atomicMax(a.absmax + leader_plane, bits);
+    } else if (active && bits) {
+      atomicMax(a.absmax + plane_id, bits);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) split_kernel(SplitArgs a) {
+  const long long per_plane = (long long)a.rows * a.d;
+  const long long n4 = (long long)a.planes_total * per_plane / 4;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n4;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long e0 = q * 4;
+    const int plane = int(e0 / per_plane);
+    const float amax = __uint_as_float(a.absmax[plane]);
+    // e: amax * 2^e in [2^14, 2^15) keeps hi within fp16 range with headroom.
+    int e = 0;
+    if (amax > 0.f && amax < INFINITY) {
+      int ex;
+      frexpf(amax, &ex);  // amax = f * 2^ex, f in [0.5, 1)
+      e = 15 - ex;
+    }
+    if (e0 % per_plane == 0) a.exp_out[plane] = e;
+    const float4 v = reinterpret_cast<const float4*>(a.in)[q];
+    const float x[4] = {ldexpf(v.x, e), ldexpf(v.y, e), ldexpf(v.z, e), ldexpf(v.w, e)};
+    __half h[4], l[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      h[t] = __float2half_rn(x[t]);
+      l[t] = __float2half_rn(x[t] - __half2float(h[t]));
+    }
+    reinterpret_cast<uint2*>(a.hi)[q] =
+        make_uint2(uint32_t(__half_as_ushort(h[0])) | (uint32_t(__half_as_ushort(h[1])) << 16),
+                   uint32_t(__half_as_ushort(h[2])) | (uint32_t(__half_as_ushort(h[3])) << 16));
+    reinterpret_cast<uint2*>(a.lo)[q] =
+        make_uint2(uint32_t(__half_as_ushort(l[0])) | (uint32_t(__half_as_ushort(l[1])) << 16),
+                   uint32_t(__half_as_ushort(l[2])) | (uint32_t(__half_as_ushort(l[3])) << 16));
+  }
+}
+
+double exact_inverse(int c) { return (c > 0 && (c & (c - 1)) == 0) ? 1.0 / double(c) : 0.0; }
+
+}  // namespace
+
+us_status launch_compress(const CompressArgs& a, cudaStream_t st) {
+  const long long total = (long long)a.B * a.planes * (a.L / a.c) * (a.d / 8);
+  const int threads = 256;
+  const long long blocks = (total + threads - 1) / threads;
+  compress_kernel<<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
+  US_LAUNCH_CHECK("compress_kernel");
+  return US_OK;
+}
+
+us_status launch_split(const SplitArgs& a, cudaStream_t st) {
+  const long long n4 = (long long)a.planes_total * a.rows * a.d / 4;
+  const int threads = 256;
+  long long blocks = (n4 + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  split_kernel<<<unsigned(blocks), threads, 0, st>>>(a);
+  US_LAUNCH_CHECK("split_kernel");
+  return US_OK;
+}
+
+}  // namespace us

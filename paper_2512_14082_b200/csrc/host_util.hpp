@@ -1,0 +1,82 @@
+// host_util.hpp — host-side helpers shared by the C-ABI translation units:
+// thread-local error text, CUDA error mapping, TMA tensor-map encoding through
+// the driver entry point (no link-time dependency on libcuda).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "../../include/us_api.h"
+
+namespace us {
+
+void set_error(const std::string& msg);
+int& launch_counter();
+
+inline us_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return US_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return US_ERR_CUDA;
+}
+
+#define US_CUDA_TRY(expr, what)                                   \
+  do {                                                            \
+    us_status _s = ::us::cuda_status((expr), what);               \
+    if (_s != US_OK) return _s;                                   \
+  } while (0)
+
+#define US_LAUNCH_CHECK(what)                                     \
+  do {                                                            \
+    ++::us::launch_counter();                                     \
+    us_status _s = ::us::cuda_status(cudaGetLastError(), what);   \
+    if (_s != US_OK) return _s;                                   \
+  } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2D row-major tensor [rows][cols] of 16-bit elements, box [box_rows][box_cols],
+// SWIZZLE_128B (box_cols * 2 must be 128 bytes).
+inline us_status make_tmap_2d_16b(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                                  uint32_t box_rows, uint32_t box_cols, bool bf16) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return US_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return US_ERR_CUDA;
+  }
+  return US_OK;
+}
+
+}  // namespace us

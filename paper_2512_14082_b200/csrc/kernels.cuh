@@ -1,0 +1,101 @@
+// kernels.cuh — launch interfaces of the hot-path kernels (device code lives in
+// compress.cu, proxy.cu, select.cu, attention.cu). All launches are
+// asynchronous on the given stream.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/us_api.h"
+
+namespace us {
+
+// ---------------------------------------------------------------- compress (a1)
+// One output plane = mean over `members` source heads of the window means of
+// `c` consecutive rows (compression.hpp:26-28 then :61-76), fp64 accumulation,
+// one f32 rounding per stage. Source head of member g of plane p is
+// (p * members + g) / div.
+struct CompressArgs {
+  const uint16_t* src;  // bf16 [B][H_src][L][d]
+  int B, H_src, L, d;
+  int c;           // window (c_q or c_k)
+  int planes;      // output planes per batch item
+  int members;     // heads pooled per plane (c_h, or 1 when deduplicated)
+  int div;         // member head -> source head divisor (G for expanded K, 1 for Q)
+  float* out;      // f32 [B][planes][L/c][d]
+  uint32_t* absmax;  // [B * planes] max |out| as f32 bits (may be null)
+};
+us_status launch_compress(const CompressArgs& a, cudaStream_t st);
+
+// f32 planes -> fp16 (hi, lo) pair scaled by 2^e (e per plane, from absmax) so
+// that hi + lo carries ~22 significant bits for the fp16x3 tensor-core proxy.
+struct SplitArgs {
+  const float* in;  // [planes_total][rows][d]
+  int planes_total, rows, d;
+  const uint32_t* absmax;  // [planes_total]
+  int* exp_out;            // [planes_total] scale exponents e
+  __half* hi;
+  __half* lo;
+};
+us_status launch_split(const SplitArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- proxy (a2-a3)
+struct ProxyArgs {
+  int B, Hc, Lq, Lk, N, D;
+  int rq, rk;          // composite rows per query block, keys per key block
+  int c_q, c_k;
+  int causal_mode;
+  int kv_planes;       // K planes per batch item
+  int kv_mul, kv_div;  // K plane of compressed head hc = hc * kv_mul / kv_div
+  const int* exp_q;    // [B*Hc]
+  const int* exp_k;    // [B*kv_planes]
+  float* lse2;         // [B][Hc][Lq] row log-sum-exp in log2 units (pass 1 out, pass 2 in)
+  float* scores;       // [B][Hc][N][N] block scores (pass 2 out; j <= i)
+  float scale_log2;    // log2(e) / sqrt(d_k)
+};
+// pass 1: per composite row lse over all (post) or live (pre) keys.
+// pass 2: per (query block, key block <= i) region sums of exp2(x - lse2).
+us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmQh, const CUtensorMap& tmQl,
+                       const CUtensorMap& tmKh, const CUtensorMap& tmKl, int pass,
+                       cudaStream_t st);
+
+// ---------------------------------------------------------------- selection (a4-a5)
+struct SelectArgs {
+  const float* scores;  // [rows][N] (row = (b*planes + p)*N + i), j <= i read
+  int rows, N, W;
+  int select_mode;
+  double P;
+  int top_k;
+  uint32_t* mask_bits;  // [rows][W]
+  int32_t* counts;      // [rows] (nullable)
+  double* coverage;     // [rows] (nullable)
+  int16_t* indices;     // [rows][N] (nullable)
+  uint32_t* err;        // device error word (bit 0: negative/NaN score)
+  int32_t* fb_count;    // fallback row counter
+  int32_t* fb_rows;     // fallback row list [rows]
+};
+us_status launch_select(const SelectArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- attention (a6)
+struct AttnArgs {
+  int B, H, H_kv, L, N, W, D;
+  int pair_heads;       // 1: CTA rows = heads (h, h+1) of one KV group; 0: blocks (i, i+1) of one head
+  int heads_per_plane;  // mask plane of head h = h / heads_per_plane
+  int planes;           // mask planes per batch item
+  const uint32_t* mask; // [B][planes][N][W] (nullptr = dense causal)
+  __nv_bfloat16* O;     // [B][H][L][D]
+  float* lse;           // [B][H][L] (nullable)
+  float scale_log2;
+};
+us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                           const CUtensorMap& tmV, cudaStream_t st);
+
+// mask validation: err |= 4 for a non-causal bit, 8 for an empty causal row;
+// first offending row index (b*planes+p)*N+i recorded with atomicMin in *first_bad.
+us_status launch_mask_check(const uint32_t* mask, int rows, int N, int W, uint32_t* err,
+                            int32_t* first_bad, cudaStream_t st);
+
+}  // namespace us

@@ -1,0 +1,341 @@
+// select.cu — per-row Top-P / top-k block selection.
+//
+// Reference semantics (selection.cpp:11-48): order = descending score, ties by
+// ascending index (stable_sort); total = fp64 sum in that order; walk the order
+// accumulating fp64 cum and stop at the first element with cum >= P * total
+// (inclusive). All-zero rows select the diagonal; P >= 1 selects the prefix.
+// top-k: the first min(k, i+1) entries of the same order.
+//
+// GPU algorithm (one warp per row, scores as f32 bit patterns in registers —
+// non-negative floats order like their unsigned bits):
+//   1. total = fp64 warp sum (fixed tree).
+//   2. binary search over the 31 value bits for v* = the largest value whose
+//      tail mass G(v*) = sum_{x >= v*} x reaches T = P * total (top-k: tail count).
+//   3. A = sum_{x > v*} x; walk the ties of v* in index order: cum = A + v*,
+//      A + 2v*, ... until cum >= T — exactly the reference walk across the
+//      boundary group.
+//   4. Certification: the reference sums sequentially in sorted order; our sums
+//      use a different (tree) order. Two fp64 summation orders of n
+//      non-negative terms differ by at most 2 n u total (u = 2^-53). Every
+//      comparison against T is therefore accepted only when its margin exceeds
+//      eps = 4 n u total; otherwise the row goes to select_fallback_kernel,
+//      which sorts the row and reproduces the reference's sequential fp64 walk
+//      verbatim. Result: masks identical to the reference rule applied to the
+//      same f32 scores, for every row (tests/test_gpu_select.py pins this).
+#include "host_util.hpp"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace us {
+namespace {
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i32(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int wpc = blockDim.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  for (long long row = (long long)blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows;
+       row += (long long)gridDim.x * wpc) {
+    const int i = int(row % a.N);
+    const int n = i + 1;
+    const float* src = a.scores + row * a.N;
+    uint32_t bits[NPL];
+    bool bad = false, nonfinite = false;
+    double part = 0.0;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      bits[k] = 0;
+      const int idx = k * 32 + lane;
+      if (k * 32 < n && idx < n) {
+        float f = __ldg(src + idx);
+        if (!(f >= 0.f)) {
+          bad = true;
+          f = 0.f;
+        }
+        if (f == 0.f) f = 0.f;  // -0 -> +0
+        if (isinf(f)) nonfinite = true;
+        bits[k] = __float_as_uint(f);
+        part += double(f);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err, 1u);
+    nonfinite = __any_sync(0xffffffffu, nonfinite);
+    const double total = warp_sum_f64(part);
+
+    uint32_t bstar = 0;     // threshold value bits
+    int ties_needed = 0;    // how many elements equal to v* (lowest index first) are taken
+    int mode = 0;           // 0: threshold rule, 1: all, 2: diagonal only
+    double cum = 0.0;
+    bool certified = true;
+    if (a.select_mode == US_SELECT_TOP_K) {
+      const int kk = min(a.top_k, n);
+      for (int bit = 30; bit >= 0; --bit) {
+        const uint32_t cand = bstar | (1u << bit);
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < NPL; ++k)
+          if (k * 32 < n) cnt += (k * 32 + lane < n && bits[k] >= cand) ? 1 : 0;
+        if (warp_sum_i32(cnt) >= kk) bstar = cand;
+      }
+      int gt = 0;
+#pragma unroll
+      for (int k = 0; k < NPL; ++k)
+        if (k * 32 < n) gt += (k * 32 + lane < n && bits[k] > bstar) ? 1 : 0;
+      ties_needed = kk - warp_sum_i32(gt);
+    } else if (!(total > 0.0)) {
+      mode = 2;
+    } else if (a.P >= 1.0) {
+      mode = 1;
+    } else if (nonfinite) {
+      certified = false;  // let the exact path handle inf arithmetic
+      mode = 1;
+    } else {
+      const double T = a.P * total;
+      for (int bit = 30; bit >= 0; --bit) {
+        const uint32_t cand = bstar | (1u << bit);
+        double g = 0.0;
+#pragma unroll
+        for (int k = 0; k < NPL; ++k)
+          if (k * 32 < n && k * 32 + lane < n && bits[k] >= cand) g += double(__uint_as_float(bits[k]));
+        if (warp_sum_f64(g) >= T) bstar = cand;
+      }
+      double A = 0.0;
+      int E = 0;
+#pragma unroll
+      for (int k = 0; k < NPL; ++k) {
+        if (k * 32 < n && k * 32 + lane < n) {
+          if (bits[k] > bstar) A += double(__uint_as_float(bits[k]));
+          if (bits[k] == bstar) ++E;
+        }
+      }
+      A = warp_sum_f64(A);
+      E = warp_sum_i32(E);
+      const double eps = 4.0 * double(n) * 0x1p-53 * total;
+      const double vstar = double(__uint_as_float(bstar));
+      cum = A;
+      certified = (T - cum) > eps;
+      int c = 0;
+      while (c < E) {
+        cum += vstar;
+        ++c;
+        if (cum >= T) break;
+        certified = certified && (T - cum) > eps;
+      }
+      certified = certified && (cum >= T) && (cum - T) > eps;
+      ties_needed = c;
+    }
+
+    // ---- emit selection
+    int tie_base = 0, sel_count = 0;
+    double sel_mass = 0.0;
+    uint32_t* mrow = a.mask_bits + row * a.W;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      if (k >= a.W) break;
+      const int idx = k * 32 + lane;
+      const bool valid = idx < n;
+      bool sel;
+      if (mode == 1) {
+        sel = valid;
+      } else if (mode == 2) {
+        sel = idx == n - 1;
+      } else {
+        const bool tie = valid && bits[k] == bstar;
+        const uint32_t tmask = __ballot_sync(0xffffffffu, tie);
+        const int rank = tie_base + __popc(tmask & lt_mask);
+        tie_base += __popc(tmask);
+        sel = valid && (bits[k] > bstar || (tie && rank < ties_needed));
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, sel);
+      if (lane == 0) mrow[k] = word;
+      if (a.indices && sel) a.indices[row * a.N + sel_count + __popc(word & lt_mask)] = int16_t(idx);
+      if (sel) sel_mass += double(__uint_as_float(bits[k]));
+      sel_count += __popc(word);
+    }
+    for (int k = NPL + lane; k < a.W; k += 32) mrow[k] = 0u;  // (never taken when NPL*32 >= N)
+    double cov;
+    if (a.select_mode == US_SELECT_TOP_K) {
+      const double m = warp_sum_f64(sel_mass);
+      cov = total > 0.0 ? m / total : 1.0;
+    } else {
+      cov = mode == 0 ? cum / total : 1.0;
+    }
+    if (lane == 0) {
+      if (a.counts) a.counts[row] = sel_count;
+      if (a.coverage) a.coverage[row] = cov;
+      if (!certified) a.fb_rows[atomicAdd(a.fb_count, 1)] = int32_t(row);
+    }
+  }
+}
+
+// Exact reference walk for uncertified rows: bitonic sort of (value desc,
+// index asc) keys in smem, then one thread sums in sorted order in fp64
+// (selection.cpp:25-46 verbatim).
+constexpr int kFbMaxN = 4096;
+__global__ void __launch_bounds__(256) select_fallback_kernel(SelectArgs a) {
+  __shared__ unsigned long long keys[kFbMaxN];
+  __shared__ uint8_t flag[kFbMaxN];
+  __shared__ int sh_k;
+  __shared__ double sh_cov;
+  const int count = *a.fb_count;
+  for (int e = blockIdx.x; e < count; e += gridDim.x) {
+    const long long row = a.fb_rows[e];
+    const int i = int(row % a.N), n = i + 1;
+    const float* src = a.scores + row * a.N;
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+      if (t < n) {
+        float f = src[t];
+        if (!(f >= 0.f) || f == 0.f) f = 0.f;
+        keys[t] = ((unsigned long long)(~__float_as_uint(f)) << 32) | unsigned(t);
+      } else {
+        keys[t] = ~0ull;
+      }
+      flag[t] = 0;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+          const int p = t ^ j;
+          if (p > t) {
+            const unsigned long long x = keys[t], y = keys[p];
+            const bool up = (t & k) == 0;
+            if ((x > y) == up) {
+              keys[t] = y;
+              keys[p] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    if (threadIdx.x == 0) {
+      auto val = [&](int t) { return double(__uint_as_float(~unsigned(keys[t] >> 32))); };
+      double total = 0.0;
+      for (int t = 0; t < n; ++t) total += val(t);
+      int ksel;
+      double cov = 1.0;
+      if (total <= 0.0) {
+        ksel = -1;  // diagonal only
+      } else if (a.P >= 1.0) {
+        ksel = n;
+      } else {
+        double cum = 0.0;
+        ksel = 0;
+        for (int t = 0; t < n; ++t) {
+          ++ksel;
+          cum += val(t);
+          if (cum >= a.P * total) break;
+        }
+        cov = cum / total;
+      }
+      sh_k = ksel;
+      sh_cov = cov;
+    }
+    __syncthreads();
+    const int ksel = sh_k;
+    if (ksel < 0) {
+      if (threadIdx.x == 0) flag[n - 1] = 1;
+    } else {
+      for (int t = threadIdx.x; t < ksel; t += blockDim.x) flag[unsigned(keys[t] & 0xFFFFFFFFu)] = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int base = 0;
+      for (int w = 0; w < a.W; ++w) {
+        const int idx = w * 32 + lane;
+        const bool sel = idx < n && flag[idx];
+        const uint32_t word = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) a.mask_bits[row * a.W + w] = word;
+        if (a.indices && sel) a.indices[row * a.N + base + __popc(word & ((1u << lane) - 1u))] = int16_t(idx);
+        base += __popc(word);
+      }
+      if (lane == 0) {
+        if (a.counts) a.counts[row] = base;
+        if (a.coverage) a.coverage[row] = sh_cov;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void mask_check_kernel(const uint32_t* mask, int rows, int N, int W, uint32_t* err,
+                                  int32_t* first_bad) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int i = int(row % N);
+  const uint32_t* m = mask + row * W;
+  bool any = false, noncausal = false;
+  for (int w = 0; w < W; ++w) {
+    uint32_t word = m[w];
+    const int lo = w * 32;
+    uint32_t causal_bits;
+    if (lo + 31 <= i) causal_bits = ~0u;
+    else if (lo > i) causal_bits = 0u;
+    else causal_bits = (i - lo == 31) ? ~0u : ((1u << (i - lo + 1)) - 1u);
+    if (word & ~causal_bits) noncausal = true;
+    if (word & causal_bits) any = true;
+  }
+  if (noncausal) {
+    atomicOr(err, 4u);
+    atomicMin(first_bad, int32_t(row));
+  }
+  if (!any) {
+    atomicOr(err, 8u);
+    atomicMin(first_bad, int32_t(row));
+  }
+}
+
+template <int NPL>
+void launch_sel(const SelectArgs& a, cudaStream_t st) {
+  const int threads = 256, wpc = threads / 32;
+  long long blocks = (a.rows + wpc - 1) / wpc;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  select_kernel<NPL><<<unsigned(blocks), threads, 0, st>>>(a);
+}
+
+}  // namespace
+
+us_status launch_select(const SelectArgs& a, cudaStream_t st) {
+  if (a.N > kFbMaxN) {
+    set_error("select: N (=L/S) above 4096 is not supported on the GPU path");
+    return US_ERR_UNSUPPORTED;
+  }
+  const int npl = (a.N + 31) / 32;
+  if (npl <= 1) launch_sel<1>(a, st);
+  else if (npl <= 2) launch_sel<2>(a, st);
+  else if (npl <= 4) launch_sel<4>(a, st);
+  else if (npl <= 8) launch_sel<8>(a, st);
+  else if (npl <= 16) launch_sel<16>(a, st);
+  else if (npl <= 32) launch_sel<32>(a, st);
+  else if (npl <= 64) launch_sel<64>(a, st);
+  else launch_sel<128>(a, st);
+  US_LAUNCH_CHECK("select_kernel");
+  if (a.select_mode == US_SELECT_TOP_P) {
+    select_fallback_kernel<<<148, 256, 0, st>>>(a);
+    US_LAUNCH_CHECK("select_fallback_kernel");
+  }
+  return US_OK;
+}
+
+us_status launch_mask_check(const uint32_t* mask, int rows, int N, int W, uint32_t* err,
+                            int32_t* first_bad, cudaStream_t st) {
+  mask_check_kernel<<<(rows + 255) / 256, 256, 0, st>>>(mask, rows, N, W, err, first_bad);
+  US_LAUNCH_CHECK("mask_check_kernel");
+  return US_OK;
+}
+
+}  // namespace us

@@ -1,0 +1,220 @@
+"""GPU parity for the individual kernels against the CPU oracle.
+
+* tcgen05 building blocks (every operand path used by proxy / attention)
+* compress: bit-exact vs the oracle's restatement of compression.hpp:13-76
+* selection: bit-exact vs top_p_row / build_block_mask on the same f32 scores
+* attention: within tolerance of the fp64 oracle on the same bf16 inputs
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+from gpu_util import to_dev_bf16
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def us():
+    import paper_2512_14082_b200 as m
+    return m
+
+
+# ------------------------------------------------------------------ tcgen05 building blocks
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("N", [64, 128])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_umma_operand_paths(mode, N, bf16):
+    g = torch.Generator().manual_seed(100 + mode * 10 + N)
+    dt = torch.bfloat16 if bf16 else torch.float16
+    A = torch.randn(128, 128, generator=g).to(dt)
+    if mode in (1, 3):
+        Bm = torch.randn(128, N, generator=g).to(dt)   # [K][N], N contiguous
+        ref = A.float() @ Bm.float()
+    else:
+        Bm = torch.randn(N, 128, generator=g).to(dt)   # [N][K]
+        ref = A.float() @ Bm.float().T
+    D = us().api.selftest_umma(mode, N, bf16, A.cuda().contiguous(), Bm.cuda().contiguous())
+    torch.cuda.synchronize()
+    err = (D.cpu() - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), f"mode {mode} N {N} bf16 {bf16}: max err {err}"
+
+
+# ------------------------------------------------------------------ compress
+@pytest.mark.parametrize("c_q,c_k,c_h,H,H_kv", [
+    (8, 8, 1, 8, 2), (4, 8, 2, 8, 2), (1, 1, 1, 4, 4), (64, 64, 4, 8, 8),
+    (8, 4, 8, 8, 2), (2, 16, 1, 4, 1), (8, 8, 2, 8, 8)])
+def test_compress_bit_exact(c_q, c_k, c_h, H, H_kv):
+    rng = np.random.default_rng(c_q * 100 + c_k * 10 + c_h)
+    B, L, d = 2, 512, 128
+    Q = O.bf16_round(rng.standard_normal((B, H, L, d)).astype(np.float32) * 3)
+    K = O.bf16_round(rng.standard_normal((B, H_kv, L, d)).astype(np.float32))
+    cfg = us().CompressionConfig(c_q=c_q, c_k=c_k, c_h=c_h)
+    Qc, Kc = us().compress(to_dev_bf16(Q), to_dev_bf16(K), cfg)
+    Qc, Kc = Qc.cpu().numpy(), Kc.cpu().numpy()
+    for b in range(B):
+        c = O.cfg(H, L, d, 64, H_kv=H_kv, c_q=c_q, c_k=c_k, c_h=c_h)
+        rq, rk = O.compress(c, Q[b], K[b])
+        assert (Qc[b].view(np.uint32) == rq.view(np.uint32)).all()
+        assert (Kc[b].view(np.uint32) == rk.view(np.uint32)).all()
+
+
+# ------------------------------------------------------------------ selection on given scores
+def _random_planes(rng, planes, N, kind):
+    s = rng.random((planes, N, N)).astype(np.float32)
+    if kind == "ties":
+        s = (np.floor(s * 4) / 4).astype(np.float32)         # many exact ties incl. zeros
+    elif kind == "skewed":
+        s = np.exp(rng.standard_normal((planes, N, N)) * 4).astype(np.float32)
+    elif kind == "zeros":
+        s[:, ::3, :] = 0.0                                   # all-zero rows -> diagonal rule
+    tri = np.tril(np.ones((N, N), bool))
+    return np.where(tri[None], s, 0).astype(np.float32)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ties", "skewed", "zeros"])
+@pytest.mark.parametrize("P", [0.3, 0.5, 0.9, 0.95, 1.0])
+@pytest.mark.parametrize("N", [5, 64, 200])
+def test_select_matches_reference_rule(kind, P, N):
+    rng = np.random.default_rng(hash((kind, P, N)) % 2**32)
+    planes = 3
+    s = _random_planes(rng, planes, N, kind)
+    cfg = us().CompressionConfig(P=P)
+    sel = us().build_block_mask(torch.from_numpy(s).cuda(), cfg, with_indices=True)
+    torch.cuda.synchronize()
+    got = sel.dense_mask()[0].cpu().numpy()
+    ref, cov = O.build_block_mask(s.astype(np.float64), planes, 1, P)
+    assert (got == ref).all(), f"{(got != ref).sum()} flips"
+    assert np.allclose(sel.coverage[0].cpu().numpy(), cov, rtol=0, atol=1e-12)
+    counts = sel.counts[0].cpu().numpy()
+    assert (counts == ref.sum(-1)).all()
+    idx = sel.indices[0].cpu().numpy()
+    for p in range(planes):
+        for i in range(N):
+            assert list(idx[p, i, : counts[p, i]]) == list(np.nonzero(ref[p, i])[0])
+
+
+@pytest.mark.parametrize("k", [1, 3, 32])
+def test_select_top_k(k):
+    rng = np.random.default_rng(k)
+    s = _random_planes(rng, 2, 100, "ties")
+    cfg = us().CompressionConfig(select_mode=us().SELECT_TOP_K, top_k=k)
+    got = us().build_block_mask(torch.from_numpy(s).cuda(), cfg).dense_mask()[0].cpu().numpy()
+    ref, _ = O.build_block_mask(s.astype(np.float64), 2, 1, 0.95, O.TOP_K, k)
+    assert (got == ref).all()
+
+
+def test_select_kat_rows():
+    # selection KATs (test_selection.cpp:33-63) as f32 rows, plus exact-tie boundary cases
+    rows = [([0.5, 0.3, 0.2], 0.7), ([0.4, 0.4, 0.2], 0.5), ([0.6, 0.4], 0.6),
+            ([0.1, 0.0, 0.9, 0.0], 1.0), ([0.0, 0.0, 0.0], 0.9), ([0.5, 0.25, 0.25], 0.5),
+            ([0.25, 0.25, 0.25, 0.25], 0.5), ([0.125] * 8, 0.75)]
+    for vals, P in rows:
+        n = len(vals)
+        s = np.zeros((1, n, n), np.float32)
+        s[0, n - 1, :] = vals
+        for i in range(n - 1):
+            s[0, i, : i + 1] = 1.0
+        sel = us().build_block_mask(torch.from_numpy(s).cuda(), us().CompressionConfig(P=P))
+        got = sel.dense_mask()[0, 0, n - 1].cpu().numpy()
+        idx, _ = O.top_p_row(np.array(vals, np.float32).astype(np.float64), P)
+        ref = np.zeros(n, bool)
+        ref[idx] = True
+        assert (got == ref).all(), (vals, P, got, ref)
+
+
+def test_select_rejects_negative_scores():
+    s = np.zeros((1, 4, 4), np.float32)
+    s[0, 2, :3] = [0.5, -0.1, 0.2]
+    s[0, np.arange(4), np.arange(4)] += 1
+    with pytest.raises(ValueError, match="nonnegative"):
+        us().build_block_mask(torch.from_numpy(s).cuda(), us().CompressionConfig(P=0.9))
+
+
+# ------------------------------------------------------------------ attention
+def _rand_qkv(rng, B, H, H_kv, L, d, scale=1.0):
+    Q = O.bf16_round(rng.standard_normal((B, H, L, d)).astype(np.float32) * scale)
+    K = O.bf16_round(rng.standard_normal((B, H_kv, L, d)).astype(np.float32))
+    V = O.bf16_round(rng.standard_normal((B, H_kv, L, d)).astype(np.float32))
+    return Q, K, V
+
+
+def _bits_from_mask(mask: np.ndarray) -> np.ndarray:
+    B, P_, N, _ = mask.shape
+    W = (N + 31) // 32
+    pad = np.zeros((B, P_, N, W * 32), bool)
+    pad[..., :N] = mask
+    w = (pad.reshape(B, P_, N, W, 32).astype(np.uint64) << np.arange(32, dtype=np.uint64)).sum(-1)
+    return w.astype(np.uint32).view(np.int32)
+
+
+# bf16 output + bf16 P: tolerance per element relative to the V scale
+ATOL, RTOL_FRO = 2e-2, 1e-2
+
+
+@pytest.mark.parametrize("H,H_kv,d", [(4, 2, 128), (4, 1, 128), (2, 2, 128), (6, 3, 64), (4, 4, 64)])
+def test_sparse_attention_random_masks(H, H_kv, d):
+    rng = np.random.default_rng(H * 10 + H_kv + d)
+    B, L = 2, 1024
+    N = L // 64
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    mask = rng.random((B, H, N, N)) < 0.4
+    tri = np.tril(np.ones((N, N), bool))
+    mask &= tri
+    mask[..., np.arange(N), np.arange(N)] |= rng.random((B, H, N)) < 0.5
+    empty = ~mask.any(-1)
+    mask[empty, 0] = True  # keep rows non-empty
+    Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V),
+                                           torch.from_numpy(_bits_from_mask(mask)).cuda())
+    Og = Og.float().cpu().numpy()
+    lseg = lseg.cpu().numpy()
+    for b in range(B):
+        Or, lser = O.block_sparse_attention(Q[b], K[b], V[b], mask[b], 64)
+        err = np.abs(Og[b] - Or)
+        assert err.max() <= ATOL, f"b={b} max_abs={err.max()}"
+        assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO
+        assert np.abs(lseg[b] - lser).max() <= 1e-3
+
+
+def test_dense_attention_matches_oracle_and_sdpa():
+    rng = np.random.default_rng(7)
+    B, H, H_kv, L, d = 1, 4, 2, 2048, 128
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    Og, lseg = us().dense_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V))
+    Og = Og.float().cpu().numpy()
+    Or, lser = O.dense_attention(Q[0], K[0], V[0])
+    assert np.abs(Og[0] - Or).max() <= ATOL
+    assert np.abs(lseg.cpu().numpy()[0] - lser).max() <= 1e-3
+    # torch fp32 reference of the same op
+    q = torch.from_numpy(Q).cuda()
+    k = torch.from_numpy(K).cuda().repeat_interleave(H // H_kv, 1)
+    v = torch.from_numpy(V).cuda().repeat_interleave(H // H_kv, 1)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True).cpu().numpy()
+    assert np.abs(Og - ref).max() <= ATOL
+
+
+def test_sparse_attention_large_logits_finite():
+    rng = np.random.default_rng(3)
+    Q, K, V = _rand_qkv(rng, 1, 2, 1, 512, 128, scale=30.0)
+    Og, lse = us().dense_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V))
+    Or, _ = O.dense_attention(Q[0], K[0], V[0])
+    assert torch.isfinite(lse).all()
+    assert np.abs(Og.float().cpu().numpy()[0] - Or).max() <= 3e-2
+
+
+def test_sparse_attention_rejects_malformed_masks():
+    rng = np.random.default_rng(5)
+    Q, K, V = _rand_qkv(rng, 1, 2, 2, 256, 64)
+    N = 4
+    m = np.tril(np.ones((1, 2, N, N), bool))
+    m[0, 1, 2, :] = False
+    with pytest.raises(ValueError, match="no selected key block"):
+        us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V),
+                                    torch.from_numpy(_bits_from_mask(m)).cuda())
+    m = np.tril(np.ones((1, 2, N, N), bool))
+    m[0, 0, 1, 3] = True
+    with pytest.raises(ValueError, match="non-causal"):
+        us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V),
+                                    torch.from_numpy(_bits_from_mask(m)).cuda())

@@ -1,0 +1,170 @@
+"""End-to-end parity of the GPU pipeline (compress -> proxy -> select -> sparse
+attention) against the CPU oracle on the reference's own workload generator.
+
+Contract (north star): block masks bit-exact vs the fp64 reference rule, any
+flipped block listed with its decision margin; outputs within the stated bf16
+tolerance. Test names mirror test_pipeline.cpp / acceptance.cpp criteria.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle_py as O
+from gpu_util import mask_margins, to_dev_bf16, workload
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+def us():
+    import paper_2512_14082_b200 as m
+    return m
+
+
+def _run_case(L, H, H_kv, d, P, mode, c_h, seed, gain=8.0, kind=O.WL_PLANTED, c_q=8, c_k=8):
+    Q, K, V, planted = workload(kind, L, H, H_kv, d, seed, gain=gain)
+    cfg = us().CompressionConfig(c_q=c_q, c_k=c_k, c_h=c_h, P=P, causal_mode=mode)
+    res = us().unisparse_attn(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1), cfg,
+                              with_scores=True)
+    torch.cuda.synchronize()
+    gpu_scores = res.report.mask.scores[0].cpu().numpy()
+    gpu_mask = res.report.mask.dense_mask()[0].cpu().numpy()
+    c = O.cfg(H, L, d, 64, H_kv=H_kv, c_q=c_q, c_k=c_k, c_h=c_h, causal_mode=mode, P=P)
+    Qc, Kc = O.compress(c, Q, K)
+    ref_scores = O.proxy_scores(c, Qc, Kc)
+    ref_mask, _ = O.build_block_mask(ref_scores, H, c_h, P)
+    return dict(Q=Q, K=K, V=V, res=res, gpu_scores=gpu_scores, gpu_mask=gpu_mask,
+                ref_scores=ref_scores, ref_mask=ref_mask, planted=planted, cfg=cfg)
+
+
+CASES = [
+    # L,    H, H_kv, d,  P,    mode,                    c_h, seed
+    (4096, 8, 2, 128, 0.95, O.POST_SOFTMAX, 1, 11),
+    (4096, 8, 2, 128, 0.90, O.POST_SOFTMAX, 1, 12),
+    (4096, 8, 2, 128, 0.95, O.PRE_SOFTMAX, 1, 13),
+    (4096, 8, 2, 128, 0.90, O.POST_SOFTMAX, 2, 14),
+    (2048, 4, 4, 64, 0.95, O.POST_SOFTMAX, 1, 15),
+    (8192, 4, 1, 128, 0.95, O.POST_SOFTMAX, 1, 16),
+]
+
+
+@pytest.mark.parametrize("L,H,H_kv,d,P,mode,c_h,seed", CASES)
+def test_masks_bit_exact_vs_reference(L, H, H_kv, d, P, mode, c_h, seed):
+    r = _run_case(L, H, H_kv, d, P, mode, c_h, seed)
+    N = L // 64
+    tri = np.tril(np.ones((N, N), bool))
+    # proxy scores: fp16x3 tensor-core proxy vs fp64 reference
+    rel = np.abs(r["gpu_scores"] - r["ref_scores"])[:, tri] / np.maximum(r["ref_scores"][:, tri], 1e-30)
+    big = r["ref_scores"][:, tri] > 1e-6
+    assert np.median(rel[big]) < 1e-5 and rel[big].max() < 1e-3, (np.median(rel[big]), rel[big].max())
+    # selection rule on the GPU's own scores == reference rule (exact)
+    mirror, _ = O.build_block_mask(r["gpu_scores"].astype(np.float64), H, c_h, P)
+    assert (mirror == r["gpu_mask"]).all()
+    # masks vs the fp64 reference: list every flipped block with its margin
+    flips = np.argwhere(r["gpu_mask"] != r["ref_mask"])
+    listed = [dict(head=int(h), **mask_margins(r["ref_scores"][h // c_h, i], P, int(i), int(j)))
+              for h, i, j in flips[:50]]
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, f"mask_flips_L{L}_H{H}_P{P}_m{mode}_ch{c_h}.json"), "w") as f:
+        json.dump({"decisions": int(H * N * (N + 1) // 2), "flips": int(len(flips)), "listed": listed}, f, indent=1)
+    assert len(flips) == 0 or all(x["mass_margin_rel"] < 1e-4 or x["score_gap_rel"] < 1e-4 for x in listed), listed
+    assert len(flips) <= max(2, H * N * (N + 1) // 2 // 20000), f"{len(flips)} flipped blocks: {listed[:5]}"
+
+
+@pytest.mark.parametrize("P,mode", [(0.95, O.POST_SOFTMAX), (0.9, O.PRE_SOFTMAX)])
+def test_output_within_tolerance(P, mode):
+    r = _run_case(4096, 4, 2, 128, P, mode, 1, 21)
+    Og = r["res"].O.float().cpu().numpy()[0]
+    # attention on the GPU's mask, computed by the fp64 oracle
+    Or, lser = O.block_sparse_attention(r["Q"], r["K"], r["V"], r["gpu_mask"], 64)
+    scale = np.abs(Or).max()
+    assert np.abs(Og - Or).max() <= 1e-2 * scale + 1e-4
+    assert np.linalg.norm(Og - Or) / np.linalg.norm(Or) <= 1e-2
+    assert np.abs(r["res"].lse.cpu().numpy()[0] - lser).max() <= 1e-3
+    # fidelity vs dense (criterion 5 analogue): cosine >= 0.99 at P=.95, >= .98 at P=.9
+    Od, _ = O.dense_attention(r["Q"], r["K"], r["V"])
+    cos = O.output_fidelity(Og, Od)["cosine"]
+    assert cos >= (0.99 if P >= 0.95 else 0.98), cos
+
+
+def test_p1_equals_dense_criterion1():
+    Q, K, V, _ = workload(O.WL_GAUSSIAN, 2048, 4, 2, 128, 31)
+    cfg = us().CompressionConfig(P=1.0)
+    res = us().unisparse_attn(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1), cfg)
+    N = 32
+    assert res.report.rho_mean == 0.0
+    assert sum(res.report.selected) == 4 * N * (N + 1) // 2
+    Od, lsed = O.dense_attention(Q, K, V)
+    assert np.abs(res.O.float().cpu().numpy()[0] - Od).max() <= 2e-2
+    Og2, _ = us().dense_attention(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1))
+    assert torch.equal(Og2, res.O)
+
+
+def test_monotone_sparsity_and_coverage_criterion4():
+    Q, K, V, _ = workload(O.WL_PLANTED, 4096, 4, 2, 128, 41)
+    prev = 1.0
+    for P in (0.7, 0.8, 0.9, 0.95, 1.0):
+        rep = us().select_blocks(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), us().CompressionConfig(P=P))
+        assert rep.rho_mean <= prev + 1e-12
+        assert rep.mask.coverage.min().item() >= P - 1e-12
+        prev = rep.rho_mean
+    assert prev == 0.0
+
+
+def test_planted_recall_criterion5():
+    Q, K, V, planted = workload(O.WL_PLANTED, 4096, 4, 2, 128, 51, gain=8.0)
+    res = us().unisparse_attn(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1),
+                              us().CompressionConfig(P=0.95))
+    m = res.report.mask.dense_mask()[0].cpu().numpy()
+    hit = tot = 0
+    for h in range(4):
+        for i in range(m.shape[1]):
+            want = [j for j in planted[h, i] if j >= 0]
+            hit += sum(m[h, i, j] for j in want)
+            tot += len(want)
+    assert hit / tot >= 0.95
+
+
+def test_top_k_mode():
+    Q, K, V, _ = workload(O.WL_PLANTED, 4096, 4, 2, 128, 61)
+    k = 8
+    cfg = us().CompressionConfig(select_mode=us().SELECT_TOP_K, top_k=k)
+    rep = us().select_blocks(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), cfg, with_scores=True)
+    got = rep.mask.dense_mask()[0].cpu().numpy()
+    c = O.cfg(4, 4096, 128, 64, H_kv=2, select_mode=O.TOP_K, top_k=k)
+    Qc, Kc = O.compress(c, Q, K)
+    ref, _ = O.build_block_mask(O.proxy_scores(c, Qc, Kc), 4, 1, 0.95, O.TOP_K, k)
+    mirror, _ = O.build_block_mask(rep.mask.scores[0].cpu().numpy().astype(np.float64), 4, 1, 0.95, O.TOP_K, k)
+    assert (mirror == got).all()
+    assert (got != ref).sum() <= 4
+    N = 64
+    assert (got.sum(-1) == np.minimum(np.arange(N) + 1, k)[None]).all()
+
+
+def test_batch_independence():
+    Q, K, V, _ = workload(O.WL_PLANTED, 2048, 4, 2, 128, 71)
+    Q2, K2, V2, _ = workload(O.WL_PLANTED, 2048, 4, 2, 128, 72)
+    cfg = us().CompressionConfig(P=0.9)
+    qb = torch.stack([to_dev_bf16(Q), to_dev_bf16(Q2)])
+    kb = torch.stack([to_dev_bf16(K), to_dev_bf16(K2)])
+    vb = torch.stack([to_dev_bf16(V), to_dev_bf16(V2)])
+    rb = us().unisparse_attn(qb, kb, vb, cfg)
+    r1 = us().unisparse_attn(qb[1:], kb[1:], vb[1:], cfg)
+    assert torch.equal(rb.O[1], r1.O[0])
+    assert torch.equal(rb.report.mask.mask_bits[1], r1.report.mask.mask_bits[0])
+
+
+def test_validation_errors_match_reference():
+    q = torch.zeros((1, 4, 1000, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="select_blocks: L=1000 not divisible by S=64"):
+        us().select_blocks(q, q, us().CompressionConfig())
+    q = torch.zeros((1, 4, 1024, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="not divisible by c_q=24"):
+        us().select_blocks(q, q, us().CompressionConfig(c_q=24))
+    q96 = torch.zeros((1, 4, 1024, 96), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(us().UnsupportedError):
+        us().select_blocks(q96, q96, us().CompressionConfig())
