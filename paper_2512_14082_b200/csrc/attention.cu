@@ -290,26 +290,28 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int c = 1; c < kBS; ++c) mx = fmaxf(mx, sv[c]);
         mx *= sl2;
-        if (mx > m_used + 8.f) {
-          if (l > 0.f) {
-            const float f = ex2_approx(m_used - mx);
-            // previous P.V (step t-1) must have retired before touching O
-            mbar_wait(&bar_pempty[(t - 1) & 1], ((t - 1) >> 1) & 1);
-            tc_fence_after();
+        const bool need = mx > m_used + 8.f;
+        const bool need_o = need && l > 0.f;  // l > 0 implies t >= 1
+        // tcgen05.ld/st are warp-collective (.sync.aligned): the O pass runs for
+        // the whole warp whenever any of its rows moves its max; other rows use f = 1.
+        if (__any_sync(0xffffffffu, need_o)) {
+          const float f = need_o ? ex2_approx(m_used - mx) : 1.f;
+          // previous P.V (step t-1) must have retired before touching O
+          mbar_wait(&bar_pempty[(t - 1) & 1], ((t - 1) >> 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
-            for (int c0 = 0; c0 < D; c0 += 16) {
-              uint32_t o[16];
-              tmem_ld16(tmem_o + lane_addr + c0, o);
-              tmem_ld_wait();
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t o[16];
+            tmem_ld16(tmem_o + lane_addr + c0, o);
+            tmem_ld_wait();
 #pragma unroll
-              for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-              tmem_st16(tmem_o + lane_addr + c0, o);
-            }
-            tmem_st_wait();
-            l *= f;
+            for (int c = 0; c < 16; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            tmem_st16(tmem_o + lane_addr + c0, o);
           }
-          m_used = mx;
+          tmem_st_wait();
+          l *= f;
         }
+        if (need) m_used = mx;
         float sum = 0.f;
 #pragma unroll
         for (int c = 0; c < kBS; c += 2) {
