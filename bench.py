@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""UniSparse prefill attention benchmark (BASELINE.json metric:
+"attention prefill ms/layer @128K; speedup vs dense FA; HBM/TC roofline %").
+
+One step = one attention layer's prefill through the B200 hot path:
+compress -> fp16x3 tcgen05 proxy -> Top-P select -> tcgen05 block-sparse
+attention, on synthetic planted-block Q/K/V (bf16, resident in HBM).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): the layer's KV-head groups are
+partitioned across ranks (strong scaling, no collective on the hot path); the
+step time is the max over ranks. Rank 0 prints ONE JSON line.
+
+--impl reference times the reference's CPU path (the oracle port in
+oracle/, the reference itself cannot be built here) on this box's host cores,
+on a bounded sample of the same workload, extrapolated to ms/layer.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (description, H, H_kv, L, d, select_mode, P/top_k)
+    "C3": ("Llama-3.1-8B-shape layer prefill bf16, L=128K, threshold (Top-P) selection", 32, 8, 131072, 128, "top_p", 0.95),
+    "C2": ("Llama-3.1-8B-shape layer prefill bf16, L=32K, top-k block selection", 32, 8, 32768, 128, "top_k", 64),
+    "C4_64K": ("Qwen2.5-7B-shape GQA prefill, L=64K, Top-P", 28, 4, 65536, 128, "top_p", 0.95),
+    "C4_128K": ("Qwen2.5-7B-shape GQA prefill, L=128K, Top-P", 28, 4, 131072, 128, "top_p", 0.95),
+    "C5": ("Video/multimodal shape, 40 heads (MHA assumed), L=256K, Top-P", 40, 40, 262144, 128, "top_p", 0.95),
+}
+DEFAULT_GAIN = {"C3": 9.0, "C2": 8.0, "C4_64K": 8.5, "C4_128K": 9.0, "C5": 9.5}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=1)
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for k, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU path
+_CPU_CACHE: dict = {}
+
+def cpu_sample(cfg_name, gain, P, seconds_target=12.0, nthreads=0, seed=2512):
+    """Times the oracle (reference CPU restatement) on a bounded sample of the
+    workload: one KV group at full length, the proxy/selection/attention for a
+    stratified sample of (head 0, query block) rows; extrapolated to ms/layer.
+    Test infrastructure only (the cpu_baseline leg)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import oracle_py as O
+    _, H, H_kv, L, d, mode, sel = CONFIGS[cfg_name]
+    G = H // H_kv
+    S, N = 64, L // 64
+    cores = nthreads or os.cpu_count()
+    t0 = time.perf_counter()
+    key = (cfg_name, gain)
+    if key not in _CPU_CACHE:
+        Q, K, V, _ = O.gen_workload(O.WL_PLANTED, L, G, d, S, 2512, H_kv=1, gain=gain, nthreads=cores)
+        _CPU_CACHE[key] = (O.bf16_round(Q), O.bf16_round(K), O.bf16_round(V))
+    Q, K, V = _CPU_CACHE[key]
+    t_gen = time.perf_counter() - t0
+    c1 = O.cfg(1, L, d, S, H_kv=1, P=P if mode == "top_p" else 0.95,
+               select_mode=O.TOP_P if mode == "top_p" else O.TOP_K, top_k=0 if mode == "top_p" else int(sel))
+    t0 = time.perf_counter()
+    Qc, Kc = O.compress(c1, Q[:1], K)
+    t_compress = time.perf_counter() - t0  # one Q head + one KV head
+    # rows: stratified over query blocks (cost grows with i)
+    rows_per_round = max(2 * cores, 8)
+    rng = np.random.default_rng(seed)
+    done_rows, t_rows = 0, 0.0
+    n_sel = 0
+    while t_rows < seconds_target and done_rows < N:
+        strata = np.linspace(0, N, rows_per_round + 1).astype(int)
+        qb = np.array([rng.integers(strata[k], max(strata[k] + 1, strata[k + 1])) for k in range(rows_per_round)],
+                      np.int32)
+        t0 = time.perf_counter()
+        srows = O.proxy_score_rows(c1, Qc, Kc, 0, qb, nthreads=cores)
+        mask = np.zeros((1, N, N), np.uint8)
+        for r, i in enumerate(qb):
+            if mode == "top_p":
+                idx, _ = O.top_p_row(srows[r, : i + 1], P)
+            else:
+                idx, _ = O.top_k_row(srows[r, : i + 1], int(sel))
+            mask[0, i, idx] = 1
+            n_sel += len(idx)
+        O.block_sparse_attention_rows(Q[:1], K, V, mask, S, np.zeros(len(qb), np.int32), qb, nthreads=cores)
+        t_rows += time.perf_counter() - t0
+        done_rows += len(qb)
+    per_row = t_rows / done_rows
+    ms_layer = 1000.0 * (t_compress * H * (1 + 1.0 / G) / 2 + per_row * H * N)
+    sample = (f"oracle (fp64 ref64 restatement) on {cores} threads: full-length compress of 1 Q + 1 KV head, "
+              f"proxy+Top-P+sparse attention for {done_rows} stratified (head 0, query block) rows of "
+              f"{cfg_name} (N={N}); extrapolated x{H * N / done_rows:.0f} rows to the {H}-head layer")
+    return ms_layer, cores, sample, {"t_rows_s": t_rows, "rows": done_rows, "t_compress_s": t_compress,
+                                     "t_gen_s": t_gen, "mean_selected_per_row": n_sel / done_rows}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gain", type=float, default=None)
+    ap.add_argument("--P", type=float, default=None)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense baselines")
+    ap.add_argument("--seed", type=int, default=2512)
+    ap.add_argument("--flashinfer", action="store_true", help="also time flashinfer dense prefill")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    desc, H, H_kv, L, d, mode, sel = CONFIGS[args.config]
+    gain = args.gain if args.gain is not None else DEFAULT_GAIN[args.config]
+    P = args.P if args.P is not None else (sel if mode == "top_p" else 0.95)
+    metric = "attention prefill ms/layer @128K; speedup vs dense FA; HBM/TC roofline %"
+    base = {"metric": metric, "unit": "ms/layer", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": f"synthetic planted_blocks (reference workloads.cpp semantics, gain={gain}, m=2, sigma=0.1), bf16"}
+    config = {"workload": desc, "config": args.config, "heads": H, "kv_heads": H_kv, "seq_len": L,
+              "head_dim": d, "block": 64, "c_q": 8, "c_k": 8, "c_h": 1,
+              "selection": f"top_p P={P}" if mode == "top_p" else f"top_k k={sel}",
+              "causal_mode": "post-softmax-block-causal", "batch": 1,
+              "parallelism": f"head-partitioned x{args.gpus} (KV groups per rank)",
+              "l2": "inputs (>=192 MB per rank) exceed the 126 MB L2; no flush needed"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        samples = []
+        info = None
+        for s in range(args.warmup + args.steps):
+            ms, cores, sample, info = cpu_sample(args.config, gain, P, seconds_target=4.0, seed=args.seed + s)
+            if s >= args.warmup:
+                samples.append(ms)
+        v = statistics.mean(samples)
+        out = dict(base, value=v, impl="reference", ms_per_step=v, config=config,
+                   cpu_baseline={"value": v, "unit": "ms/layer", "cores": cores, "kind": "port", "sample": sample},
+                   e2e={"value": v, "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   gpu_launches=0, detail=info)
+        print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    import paper_2512_14082_b200 as us
+    from paper_2512_14082_b200 import workloads
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    if H_kv % world != 0:
+        raise SystemExit(f"H_kv={H_kv} not divisible by {world} GPUs")
+    kv_per = H_kv // world
+    G = H // H_kv
+    heads = list(range(rank * kv_per * G, (rank + 1) * kv_per * G))
+    Q, K, V = workloads.planted_blocks(L, H, H_kv, d, 64, seed=args.seed, gain=gain, heads=heads)
+    torch.cuda.synchronize()
+    cfg = us.CompressionConfig(P=P) if mode == "top_p" else us.CompressionConfig(
+        select_mode=us.SELECT_TOP_K, top_k=int(sel))
+    eng = us.Engine(Q, K, V, cfg)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up + validity check (errors surface here, outside the timed region)
+    for _ in range(max(args.warmup, 1)):
+        eng.run()
+    torch.cuda.synchronize()
+    us.api._raise(us.api.lib().us_check_device_errors(us.api.C.byref(eng.p), us.api._ptr(eng.ws), us.api._stream()))
+    launches_per_step = eng.launches()
+    N = L // 64
+    selected = int(eng.sel.counts.to(torch.int64).sum().item())
+    causal = len(heads) * N * (N + 1) // 2
+    rho = 1.0 - selected / causal
+
+    # ---------------------------------------------------------------- timed region (device)
+    stream = torch.cuda.current_stream()
+    us.api.profile_enable(args.steps)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        eng.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    stages = us.api.profile_read(args.steps)
+    us.api.profile_disable()
+    ms = max_over_ranks(ms_local)
+    stage_ms = {k: statistics.mean(s[k] for s in stages) for k in us.api.STAGES}
+
+    # ---------------------------------------------------------------- e2e (host buffers)
+    Qh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True).copy_(Q)
+    Kh = torch.empty(K.shape, dtype=K.dtype, pin_memory=True).copy_(K)
+    Vh = torch.empty(V.shape, dtype=V.dtype, pin_memory=True).copy_(V)
+    Oh = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        eng.Q.copy_(Qh, non_blocking=True)
+        eng.K.copy_(Kh, non_blocking=True)
+        eng.V.copy_(Vh, non_blocking=True)
+        eng.run()
+        Oh.copy_(eng.O, non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.steps)
+    h2d = (Q.numel() + K.numel() + V.numel()) * 2 * world
+    d2h = Q.numel() * 2 * world
+
+    # ---------------------------------------------------------------- dense baselines (same shard)
+    dense = {}
+    if not args.no_dense:
+        def timeit(fn, iters=3):
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(iters):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / iters
+        dense["ours_p1"] = max_over_ranks(timeit(lambda: eng.run(dense=True)))
+        try:
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+            with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+                dense["cudnn_sdpa"] = max_over_ranks(timeit(lambda: torch.nn.functional.scaled_dot_product_attention(
+                    Q, K, V, is_causal=True, enable_gqa=True)))
+        except Exception as e:  # pragma: no cover
+            log("cudnn sdpa unavailable:", e)
+        try:
+            if not args.flashinfer:
+                raise RuntimeError("skipped (enable with --flashinfer; JIT-compiles on first use)")
+            import flashinfer
+            q3, k3, v3 = Q[0].transpose(0, 1).contiguous(), K[0].transpose(0, 1).contiguous(), V[0].transpose(0, 1).contiguous()
+            dense["flashinfer"] = max_over_ranks(timeit(lambda: flashinfer.single_prefill_with_kv_cache(
+                q3, k3, v3, causal=True)))
+        except Exception as e:  # pragma: no cover
+            log("flashinfer unavailable:", e)
+    fastest = min(dense.items(), key=lambda kv: kv[1]) if dense else None
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+    flops_attn = selected * 4 * 64 * 64 * d
+    dominant = max(stage_ms.items(), key=lambda kv: kv[1])[0]
+    if dominant == "attention":
+        achieved = flops_attn / (stage_ms["attention"] * 1e-3) / 1e12
+        roof = {"kernel": "attn_kernel (tcgen05 block-sparse FA)", "bound": "tensor", "achieved": achieved,
+                "peak": tf_sust, "unit": "TFLOP/s", "frac": achieved / tf_sust}
+    else:
+        Lq = L // 8
+        fl = 3 * 2 * Lq * Lq * len(heads) * d * 1.5  # fp16x3, post-softmax: full-square lse pass + causal pass
+        achieved = fl / (stage_ms["proxy"] * 1e-3) / 1e12
+        roof = {"kernel": "proxy_kernel (tcgen05 fp16x3)", "bound": "tensor", "achieved": achieved, "peak": tf_sust,
+                "unit": "TFLOP/s", "frac": achieved / tf_sust}
+    roof["traffic"] = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        roof["traffic"] = json.load(open(tp)).get(args.config, {}).get(roof["kernel"].split()[0])
+    roof["peak_source"] = f"MEASURED_PEAKS.json ({peak_src}, sustained bf16)"
+    comp_bytes = (len(heads) + len(heads) // G) * L * d * 2 + (len(heads) + len(heads) // G) * (L // 8) * d * 4
+    stage_roofs = {
+        "compress": {"bound": "hbm", "bytes": comp_bytes,
+                     "achieved_gbs": comp_bytes / (stage_ms["compress"] * 1e-3) / 1e9, "peak_gbs": hbm},
+        "attention": {"bound": "tensor", "flops": flops_attn,
+                      "achieved_tflops": flops_attn / (stage_ms["attention"] * 1e-3) / 1e12, "peak_tflops": tf_sust},
+    }
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, cores, sample, info = cpu_sample(args.config, gain, P)
+        cpu = {"value": v, "unit": "ms/layer", "cores": cores, "kind": "port", "sample": sample}
+    out = dict(base, value=ms, ms_per_step=ms, config=config, clocks=clk,
+               e2e={"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+               gpu_launches=launches_per_step * args.steps,
+               roofline=roof, cpu_baseline=cpu,
+               stages_ms=stage_ms, stage_roofline=stage_roofs,
+               sparsity={"rho": rho, "selected_blocks": selected, "causal_blocks": causal},
+               dense_baselines_ms=dense,
+               speedup_vs_dense={"vs": fastest[0], "dense_ms": fastest[1], "speedup": fastest[1] / ms} if fastest else None)
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -152,6 +152,15 @@ us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, 
 /* Number of kernel launches the last successful call on this thread issued. */
 int32_t us_last_launch_count(void);
 
+/* Per-stage CUDA-event timing (observability). While enabled, each
+ * us_unisparse_attention call on this thread records events on its stream at
+ * the stage boundaries [compress+split | proxy | select | attention] into the
+ * next of `max_calls` slots. us_profile_read synchronizes on the recorded
+ * events and writes [calls][4] stage times in ms; returns the number of calls. */
+us_status us_profile_enable(int32_t max_calls);
+int32_t us_profile_read(float* ms_out, int32_t max_calls);
+void us_profile_disable(void);
+
 #ifdef __cplusplus
 }
 #endif

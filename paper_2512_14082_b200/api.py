@@ -106,6 +106,9 @@ def lib() -> C.CDLL:
             L.us_selection_flops.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp]
             L.us_selftest_umma.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]
             L.us_last_launch_count.restype = C.c_int32
+            L.us_profile_enable.argtypes = [C.c_int32]
+            L.us_profile_read.argtypes = [C.c_void_p, C.c_int32]
+            L.us_profile_read.restype = C.c_int32
         return _lib
 
 
@@ -376,3 +379,22 @@ def selftest_umma(mode: int, N: int, bf16: bool, A: torch.Tensor, B: torch.Tenso
     D = torch.empty((128, N), dtype=torch.float32, device=A.device)
     _raise(lib().us_selftest_umma(mode, N, int(bf16), _ptr(A), _ptr(B), _ptr(D), _stream()))
     return D
+
+
+STAGES = ("compress", "proxy", "select", "attention")
+
+
+def profile_enable(max_calls: int):
+    """Record per-stage CUDA events for the next max_calls unisparse_attn calls."""
+    _raise(lib().us_profile_enable(max_calls))
+
+
+def profile_read(max_calls: int):
+    """-> list of per-call dicts {stage: ms} (synchronizes on the recorded events)."""
+    buf = (C.c_float * (4 * max_calls))()
+    n = lib().us_profile_read(C.cast(buf, C.c_void_p), max_calls)
+    return [{k: buf[c * 4 + i] for i, k in enumerate(STAGES)} for c in range(n)]
+
+
+def profile_disable():
+    lib().us_profile_disable()

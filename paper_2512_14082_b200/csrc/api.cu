@@ -23,6 +23,17 @@ namespace us {
 namespace {
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+
+// stage-boundary events: slot c uses events [5c, 5c+5)
+struct Profiler {
+  std::vector<cudaEvent_t> ev;
+  int max_calls = 0, next = 0;
+  bool on() const { return max_calls > 0; }
+  void mark(int call, int k, cudaStream_t st) {
+    if (call >= 0 && call < max_calls) cudaEventRecord(ev[size_t(call) * 5 + k], st);
+  }
+};
+thread_local Profiler g_prof;
 }  // namespace
 
 void set_error(const std::string& msg) { g_err = msg; }
@@ -194,7 +205,8 @@ us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, s
 }
 
 // compress + split + proxy (pass 1, 2) into ws.scores.
-us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, cudaStream_t st) {
+us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, cudaStream_t st,
+                    int prof_call = -1) {
   Geo g(p);
   Ws w = layout(p);
   US_CUDA_TRY(cudaMemsetAsync(ws, 0, w.header_bytes, st), "workspace clear");
@@ -213,6 +225,7 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
                at<int>(ws, w.exp_k), at<__half>(ws, w.kh), at<__half>(ws, w.kl)};
   if ((s = launch_split(sk, st)) != US_OK) return s;
 
+  g_prof.mark(prof_call, 1, st);
   const uint64_t qrows = uint64_t(g.B) * g.Hc * g.Lq + 128, krows = uint64_t(g.B) * g.kv_planes * g.Lk + 128;
   CUtensorMap tQh, tQl, tKh, tKl;
   if ((s = make_tmap_2d_16b(&tQh, at<void>(ws, w.qh), qrows, g.D, 128, 64, false)) != US_OK) return s;
@@ -327,6 +340,36 @@ const char* us_version(void) { return "unisparse-b200 0.1 (sm_100a)"; }
 const char* us_last_error(void) { return g_err.c_str(); }
 int32_t us_last_launch_count(void) { return g_launches; }
 
+us_status us_profile_enable(int32_t max_calls) {
+  us_profile_disable();
+  if (max_calls <= 0) return US_OK;
+  g_prof.ev.resize(size_t(max_calls) * 5);
+  for (auto& e : g_prof.ev) US_CUDA_TRY(cudaEventCreate(&e), "us_profile_enable");
+  g_prof.max_calls = max_calls;
+  g_prof.next = 0;
+  return US_OK;
+}
+
+int32_t us_profile_read(float* ms_out, int32_t max_calls) {
+  const int n = std::min(std::min(g_prof.next, g_prof.max_calls), int(max_calls));
+  for (int c = 0; c < n; ++c) {
+    cudaEventSynchronize(g_prof.ev[size_t(c) * 5 + 4]);
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, g_prof.ev[size_t(c) * 5 + k], g_prof.ev[size_t(c) * 5 + k + 1]);
+      ms_out[c * 4 + k] = ms;
+    }
+  }
+  return n;
+}
+
+void us_profile_disable(void) {
+  for (auto& e : g_prof.ev) cudaEventDestroy(e);
+  g_prof.ev.clear();
+  g_prof.max_calls = 0;
+  g_prof.next = 0;
+}
+
 int us_validate(const us_params* p, char* msg, size_t cap) {
   if (!p) return 1;
   Checked c = check(*p, true);
@@ -435,7 +478,10 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
   Geo g(*p);
   Ws w = layout(*p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((s = run_proxy(*p, Q, K, workspace, st)) != US_OK) return s;
+  const int call = g_prof.on() ? g_prof.next++ : -1;
+  g_prof.mark(call, 0, st);
+  if ((s = run_proxy(*p, Q, K, workspace, st, call)) != US_OK) return s;
+  g_prof.mark(call, 2, st);
   if (sel && sel->scores)
     US_CUDA_TRY(cudaMemcpyAsync(sel->scores, at<float>(workspace, w.scores),
                                 size_t(4) * g.B * g.Hc * g.N * g.N, cudaMemcpyDeviceToDevice, st),
@@ -443,9 +489,9 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
   uint32_t* mask = (sel && sel->mask_bits) ? sel->mask_bits : at<uint32_t>(workspace, w.mask);
   if ((s = run_select_rows(*p, at<float>(workspace, w.scores), g.Hc, mask, sel, workspace, st)) != US_OK)
     return s;
-  const int launches = g_launches;
+  g_prof.mark(call, 3, st);
   if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st)) != US_OK) return s;
-  (void)launches;
+  g_prof.mark(call, 4, st);
   if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "unisparse_attn");
   return US_OK;
 }

@@ -172,6 +172,26 @@ __global__ void __launch_bounds__(192, 1)
     const float lse2 = (PASS == 2 && row_ok) ? a.lse2[(long long)plane * a.Lq + t_row] : 0.f;
     const int i_row = t_row / a.rq;
     float gacc = 0.f;  // rk > 32: a key block spans several 32-column chunks
+    // Sum one key-block partial over the rq rows of the query block (fixed
+    // shuffle tree; smem across warps when rq > 32) and store Score(i, j), j <= i.
+    auto emit = [&](float s, int j) {
+      if (a.rq <= 32) {
+        for (int o = 1; o < a.rq; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (row_ok && (lane % a.rq) == 0 && j <= i_row)
+          a.scores[((long long)plane * a.N + i_row) * a.N + j] = s;
+      } else {
+        for (int o = 1; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[q][0] = s;
+        named_bar_sync(1, 128);
+        const int wpb = a.rq / 32;  // warps per query block
+        if (lane == 0 && (q % wpb) == 0) {
+          float tot = 0.f;
+          for (int w = 0; w < wpb; ++w) tot += red[q + w][0];
+          if (row_ok && j <= i_row) a.scores[((long long)plane * a.N + i_row) * a.N + j] = tot;
+        }
+        named_bar_sync(1, 128);
+      }
+    };
 
     for (int t = 0; t < n_tiles; ++t) {
       const int buf = t & 1;
@@ -205,60 +225,32 @@ __global__ void __launch_bounds__(192, 1)
             m = m_new;
           }
         } else {
-          float p[32];
+          float v32[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            p[c] = (key0 + c < live) ? ex2_approx(fmaf(__uint_as_float(v[c]), k2, -lse2)) : 0.f;
+            v32[c] = (key0 + c < live) ? ex2_approx(fmaf(__uint_as_float(v[c]), k2, -lse2)) : 0.f;
+          // pairwise tree inside groups of rk keys (register indices are compile-time;
+          // the runtime rk only predicates whole levels)
+#pragma unroll
+          for (int w = 1; w < 32; w <<= 1) {
+            if (w < a.rk) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 2 * w) v32[c] += v32[c + w];
+            }
+          }
           if (a.rk <= 32) {
-            // groups of rk keys inside this chunk, then reduce over rq rows
-            const int ng = 32 / a.rk;
-            for (int g = 0; g < ng; ++g) {
-              float s = 0.f;
-              for (int c = g * a.rk; c < (g + 1) * a.rk; ++c) s += p[c];
-              if (a.rq <= 32) {
-                for (int o = 1; o < a.rq; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                const int j = (key0 + g * a.rk) / a.rk;
-                if (row_ok && (lane % a.rq) == 0 && j <= i_row)
-                  a.scores[((long long)plane * a.N + i_row) * a.N + j] = s;
-              } else {
-                for (int o = 1; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if (lane == 0) red[q][0] = s;
-                named_bar_sync(1, 128);
-                const int wpb = a.rq / 32;  // warps per query block
-                if (lane == 0 && (q % wpb) == 0) {
-                  float tot = 0.f;
-                  for (int w = 0; w < wpb; ++w) tot += red[q + w][0];
-                  const int j = (key0 + g * a.rk) / a.rk;
-                  if (row_ok && j <= i_row) a.scores[((long long)plane * a.N + i_row) * a.N + j] = tot;
-                }
-                named_bar_sync(1, 128);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              if ((c & (a.rk - 1)) == 0) {  // warp-uniform
+                const int j = (key0 + c) / a.rk;
+                emit(v32[c], j);
               }
             }
           } else {
-            float s = 0.f;
-#pragma unroll
-            for (int c = 0; c < 32; ++c) s += p[c];
-            gacc += s;
+            gacc += v32[0];
             if (((key0 + 32) % a.rk) == 0) {
-              float tot = gacc;
+              emit(gacc, key0 / a.rk);
               gacc = 0.f;
-              const int j = key0 / a.rk;
-              if (a.rq <= 32) {
-                for (int o = 1; o < a.rq; o <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-                if (row_ok && (lane % a.rq) == 0 && j <= i_row)
-                  a.scores[((long long)plane * a.N + i_row) * a.N + j] = tot;
-              } else {
-                for (int o = 1; o < 32; o <<= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-                if (lane == 0) red[q][0] = tot;
-                named_bar_sync(1, 128);
-                const int wpb = a.rq / 32;
-                if (lane == 0 && (q % wpb) == 0) {
-                  float t2 = 0.f;
-                  for (int w = 0; w < wpb; ++w) t2 += red[q + w][0];
-                  if (row_ok && j <= i_row) a.scores[((long long)plane * a.N + i_row) * a.N + j] = t2;
-                }
-                named_bar_sync(1, 128);
-              }
             }
           }
         }
