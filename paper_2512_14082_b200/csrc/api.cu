@@ -298,6 +298,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.heads_per_plane = hpp;
   a.planes = g.H / hpp;
   a.mask = mask;
+  a.Q = static_cast<const __nv_bfloat16*>(Q);
   a.O = static_cast<__nv_bfloat16*>(O);
   a.lse = lse;
   a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));

@@ -86,6 +86,7 @@ struct AttnArgs {
   int heads_per_plane;  // mask plane of head h = h / heads_per_plane
   int planes;           // mask planes per batch item
   const uint32_t* mask; // [B][planes][N][W] (nullptr = dense causal)
+  const __nv_bfloat16* Q; // [B][H][L][D] (rows go straight to TMEM)
   __nv_bfloat16* O;     // [B][H][L][D]
   float* lse;           // [B][H][L] (nullable)
   float scale_log2;

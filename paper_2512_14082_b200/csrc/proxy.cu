@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar_q, bar_kfull[kStages], bar_kempty[kStages], bar_sfull[2], bar_sempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float red[4][32];
+  __shared__ float red[kRows][33];  // pass 2: per-row key-group partials of one segment
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int rt = gridDim.x - 1 - blockIdx.x;  // heavy (late) row tiles first
@@ -170,29 +170,6 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t lane_addr = tmem + (uint32_t(q * 32) << 16);
     float m = -INFINITY, l = 0.f;
     const float lse2 = (PASS == 2 && row_ok) ? a.lse2[(long long)plane * a.Lq + t_row] : 0.f;
-    const int i_row = t_row / a.rq;
-    float gacc = 0.f;  // rk > 32: a key block spans several 32-column chunks
-    // Sum one key-block partial over the rq rows of the query block (fixed
-    // shuffle tree; smem across warps when rq > 32) and store Score(i, j), j <= i.
-    auto emit = [&](float s, int j) {
-      if (a.rq <= 32) {
-        for (int o = 1; o < a.rq; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (row_ok && (lane % a.rq) == 0 && j <= i_row)
-          a.scores[((long long)plane * a.N + i_row) * a.N + j] = s;
-      } else {
-        for (int o = 1; o < 32; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) red[q][0] = s;
-        named_bar_sync(1, 128);
-        const int wpb = a.rq / 32;  // warps per query block
-        if (lane == 0 && (q % wpb) == 0) {
-          float tot = 0.f;
-          for (int w = 0; w < wpb; ++w) tot += red[q + w][0];
-          if (row_ok && j <= i_row) a.scores[((long long)plane * a.N + i_row) * a.N + j] = tot;
-        }
-        named_bar_sync(1, 128);
-      }
-    };
-
     for (int t = 0; t < n_tiles; ++t) {
       const int buf = t & 1;
       mbar_wait(&bar_sfull[buf], (t / 2) & 1);
@@ -229,8 +206,8 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c)
             v32[c] = (key0 + c < live) ? ex2_approx(fmaf(__uint_as_float(v[c]), k2, -lse2)) : 0.f;
-          // pairwise tree inside groups of rk keys (register indices are compile-time;
-          // the runtime rk only predicates whole levels)
+          // pairwise tree inside groups of min(rk, 32) keys (register indices are
+          // compile-time; the runtime rk only predicates whole levels)
 #pragma unroll
           for (int w = 1; w < 32; w <<= 1) {
             if (w < a.rk) {
@@ -238,20 +215,37 @@ __global__ void __launch_bounds__(192, 1)
               for (int c = 0; c < 32; c += 2 * w) v32[c] += v32[c + w];
             }
           }
+          // stage this row's key-group partials of the current segment in smem
+          const int cps = min(4, a.rk);            // chunks per segment
+          const int gseg = (32 * cps) / a.rk;      // key groups per segment (<= 32)
+          const int cseg = ch % cps;               // chunk index inside the segment
           if (a.rk <= 32) {
+            const int ng = 32 / a.rk;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              if ((c & (a.rk - 1)) == 0) {  // warp-uniform
-                const int j = (key0 + c) / a.rk;
-                emit(v32[c], j);
-              }
-            }
+            for (int c = 0; c < 32; ++c)
+              if ((c & (a.rk - 1)) == 0) red[row][cseg * ng + c / a.rk] = v32[c];
           } else {
-            gacc += v32[0];
-            if (((key0 + 32) % a.rk) == 0) {
-              emit(gacc, key0 / a.rk);
-              gacc = 0.f;
+            const int gi = (cseg * 32) / a.rk;     // group inside the segment
+            if ((cseg * 32) % a.rk == 0) red[row][gi] = v32[0];
+            else red[row][gi] += v32[0];
+          }
+          if (cseg == cps - 1) {
+            // cross-row sums over the rq rows of each query block, fixed order,
+            // consecutive threads -> consecutive key blocks (coalesced stores)
+            named_bar_sync(1, 128);
+            const int qb_tile = kRows / a.rq;
+            const int nout = qb_tile * gseg;
+            const int j0 = (t * kKeys + (ch - cseg) * 32) / a.rk;
+            for (int o = row; o < nout; o += 128) {
+              const int qb = o / gseg, gg = o % gseg;
+              float sum = 0.f;
+              for (int r = 0; r < a.rq; ++r) sum += red[qb * a.rq + r][gg];
+              const int i = (r0 / a.rq) + qb;
+              const int j = j0 + gg;
+              if (qb * a.rq + r0 < a.Lq && j <= i)
+                a.scores[((long long)plane * a.N + i) * a.N + j] = sum;
             }
+            named_bar_sync(1, 128);
           }
         }
       }
