@@ -28,7 +28,7 @@ from typing import Optional
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_build", "libunisparse_b200.so")
+LIB_PATH = os.environ.get("US_LIB_PATH_OVERRIDE") or os.path.join(_PKG, "_build", "libunisparse_b200.so")
 
 US_OK, US_ERR_INVALID_ARGUMENT, US_ERR_UNSUPPORTED, US_ERR_CUDA, US_ERR_INVALID_MASK, \
     US_ERR_NONFINITE, US_ERR_WORKSPACE = range(7)

@@ -294,7 +294,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.N = g.N;
   a.W = g.W;
   a.D = g.D;
-  a.pair_heads = (g.G % 2 == 0) ? 1 : 0;
+  a.group_mode = (g.G % 4 == 0) ? 0 : (g.G == 2 ? 1 : 2);
   a.heads_per_plane = hpp;
   a.planes = g.H / hpp;
   a.mask = mask;

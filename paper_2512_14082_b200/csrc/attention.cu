@@ -7,48 +7,78 @@
 // online softmax (running max, rescaled denominator and accumulator), then
 // O = acc / den and lse = m + log(den).
 //
-// CTA tile (M = 128 rows = one UMMA M):
-//   rows   0..63  = group 0 = (head h0, query block i0)
-//   rows  64..127 = group 1 = (head h1, query block i1)
-// with both groups reading the SAME KV head, so every K/V tile staged in smem
-// feeds both halves of one M=128 MMA (GQA head sharing). Pairing: heads
-// (2p, 2p+1) of one KV group at the same query block when H/H_kv is even,
-// else query blocks (2p, 2p+1) of one head. The CTA walks the ascending union
-// of the two groups' selected blocks; a group that did not select block j
-// contributes P = 0 rows (no exp work, no statistics update), so the output
-// equals per-group sparse attention over exactly its own selected blocks.
+// CTA = 4 "groups" (head, query block) that read the SAME KV head, as two
+// UMMA M=128 tiles: tile A = groups 0,1 (rows 0-63 | 64-127), tile B = groups 2,3.
+//   H/H_kv % 4 == 0 : 4 consecutive heads of a KV group at one query block
+//   H/H_kv == 2     : both heads of the group at query blocks (i, i-1)
+//   otherwise       : one head at 4 consecutive query blocks
+// Every K/V tile staged in smem feeds up to 2 x 128 query rows (halving the
+// L2->SM K/V traffic per FLOP of a 128-row design, which was the measured
+// limit), and each tile only runs S/P.V for the union of ITS two groups'
+// selected blocks; K/V is loaded for the union of all four. A group that did
+// not select a block visited by its tile contributes P = 0 rows, so each
+// group's output equals sparse attention over exactly its own selection.
 //
-// Roles (256 threads): warp 0 TMA producer (Q once, K/V ring of 4 stages),
-// warp 1 MMA issuer and TMEM owner, warps 2-3 load the mask rows, warps 4-7
-// softmax + epilogue (thread = row = TMEM lane).
-// TMEM (256 cols): S double buffer [0,128) (2 x 64 fp32 cols), O [128,128+D).
-// P goes registers -> bf16 -> 128B-swizzled smem (K-major A operand of P.V);
-// V is the MN-major B operand straight from its row-major TMA tile.
+// Roles (384 threads): warp 0 TMA producer (6-stage K/V ring), warps 1 / 3
+// MMA issuers of tile A / B (warp 1 owns TMEM), warp 2 builds the union list,
+// warps 4-7 softmax of tile A, warps 8-11 softmax of tile B (thread = row).
+// TMEM per tile X (256 cols at X*256): S [0,64) fp32 with P (bf16x2) aliased
+// into [0,32) after the row is read, O [64,192), Q [192,256) (bf16x2, A operand
+// of S = Q K^T). Both MMAs are TS-mode (A from TMEM); only K/V come from smem.
+// Per tile the tensor pipe runs ... S(k) | P.V(k) S(k+1) | P.V(k+1) ... in
+// issue order; the two tiles ping-pong so one softmax overlaps the other
+// tile's MMAs (the tile issuers are independent warps). The S(k+1) commit retires P.V(k) too (commit covers all prior
+// MMAs), so O rescales and P/S aliasing need no extra barriers.
 // Online softmax in log2 units with lazy rescaling: the running max used for
-// exponentiation only moves when a row max exceeds it by > 8 (p <= 2^8), and
-// only then is the O row in TMEM rescaled (after the previous P.V retires).
+// exponentiation only moves when a row max exceeds it by > 8 (p <= 2^8).
 #include "host_util.hpp"
 #include "kernels.cuh"
 #include "ptx.cuh"
 
+#ifndef US_ATTN_SKELETON
+#define US_ATTN_SKELETON 0
+#endif
+// Debug timeline (tools/attn_trace.py): per step k of tile x of the traced CTA,
+// clock64 at [S issued, S seen by softmax, P ready, P.V issued].
+#ifndef US_ATTN_TRACE
+#define US_ATTN_TRACE 0
+#endif
+#if US_ATTN_TRACE
+__device__ long long g_attn_trace[2 * 4096 * 8];
+__device__ int g_attn_trace_cta;
+#define TRACE(x, k, e)                                                                  \
+  do {                                                                                  \
+    if (blockIdx.x == g_attn_trace_cta && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 8 + (e)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(x, k, e) \
+  do {                 \
+  } while (0)
+#endif
+
 namespace us {
 namespace {
 
-constexpr int kBM = 128;   // rows per CTA
-constexpr int kBS = 64;    // block size (keys per tile, rows per group)
-constexpr int kST = 4;     // K/V stages
-constexpr int kMaxW = 128; // mask words per row (N <= 4096)
+constexpr int kBS = 64;     // block size (keys per tile, rows per group)
+constexpr int kMaxN = 4096; // blocks per row
+constexpr int kMaxW = kMaxN / 32;
+
+// K/V ring depth: a 64-key K+V tile takes ~1-2 us to land from L2, so the ring
+// must cover several steps of prefetch.
+template <int D>
+constexpr int stages_for() { return D == 128 ? 6 : 10; }
 
 template <int D>
 struct AttnSmem {
+  static constexpr int kST = stages_for<D>();
   static constexpr int kChunks = D / 64;
-  static constexpr int kKVBytes = kBS * D * 2;         // one of K / V per stage
-  static constexpr int kK = 0;                         // stage s: K at kK + s*2*kKVBytes, V after
-  static constexpr int kBytes = kK + kST * 2 * kKVBytes;
+  static constexpr int kKVBytes = kBS * D * 2;  // one of K / V per stage
+  static constexpr int kBytes = kST * 2 * kKVBytes;
 };
 
-// TMEM columns (512 allocated): S0 S1 | O0 | O1 | Q (bf16x2 packed) | P0 P1 (bf16x2 packed)
-constexpr uint32_t kTS = 0, kTO = 128, kTQ = 384, kTP = 448;
+// TMEM columns of tile X start at X * 256: S [0,64) (P aliased into [0,32)),
+// O [64, 64+D), Q [192, 192+D/2).
+constexpr uint32_t kTS = 0, kTO = 64, kTQ = 192;
 
 // exp2 on the FMA/ALU pipes for a pair of values (offloads MUFU): round-to-nearest
 // split x = n + f, f in [-0.5, 0.5], cubic minimax for 2^f (max rel. err 7.7e-5,
@@ -67,84 +97,105 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-constexpr int kPolyFrom = 24;  // columns [24, 32) of a warpgroup half-tile use ex2_poly2 (25%)
+constexpr int kPolyFrom = 48;  // columns [48, 64) of an off-diagonal tile use ex2_poly2 (25%)
+
+struct Groups {
+  int b, h[4], i[4];
+  bool en[4];
+};
+
+__device__ __forceinline__ Groups decode_item(const AttnArgs& a, int item) {
+  Groups g;
+  const int G = a.H / a.H_kv;
+  if (a.group_mode == 0) {  // 4 heads of a KV group, one query block
+    const int quads = a.H / 4;
+    const int per_i = a.B * quads;
+    const int i = a.N - 1 - item / per_i;
+    const int rem = item % per_i;
+    g.b = rem / quads;
+    const int h0 = (rem % quads) * 4;
+    for (int k = 0; k < 4; ++k) {
+      g.h[k] = h0 + k;
+      g.i[k] = i;
+      g.en[k] = true;
+    }
+  } else if (a.group_mode == 1) {  // 2 heads x query blocks (i, i-1)
+    const int npairs = (a.N + 1) / 2;
+    const int per_ip = a.B * a.H_kv;
+    const int ip = npairs - 1 - item / per_ip;
+    const int rem = item % per_ip;
+    g.b = rem / a.H_kv;
+    const int h0 = (rem % a.H_kv) * G;
+    const int ib = 2 * ip + 1, ia = 2 * ip;
+    for (int k = 0; k < 4; ++k) {
+      g.h[k] = h0 + (k & 1);
+      g.i[k] = k < 2 ? ib : ia;
+    }
+    for (int k = 0; k < 4; ++k) g.en[k] = g.i[k] < a.N;
+  } else {  // one head, 4 query blocks
+    const int nq = (a.N + 3) / 4;
+    const int per_q = a.B * a.H;
+    const int iq = nq - 1 - item / per_q;
+    const int rem = item % per_q;
+    g.b = rem / a.H;
+    for (int k = 0; k < 4; ++k) {
+      g.h[k] = rem % a.H;
+      g.i[k] = 4 * iq + 3 - k;
+      g.en[k] = g.i[k] < a.N;
+    }
+  }
+  return g;
+}
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using SL = AttnSmem<D>;
+  constexpr int kST = SL::kST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q, bar_kvfull[kST], bar_kvempty[kST], bar_sfull[2], bar_sempty[2],
-      bar_pfull[2], bar_pempty[2], bar_ofull;
+  __shared__ uint64_t bar_q[2], bar_kvfull[kST], bar_kvempty[kST], bar_sfull[2], bar_pfull[2], bar_ofull[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int n_steps_sh;
-  __shared__ uint32_t mrow[2][kMaxW];
-  // union of the two groups' selected blocks, ascending: j | sel0 << 16 | sel1 << 17
-  __shared__ uint32_t steps[kMaxW * 32];
-  __shared__ float xm[2][kBM], xl[2][kBM];
+  __shared__ uint32_t mrow[4][kMaxW];
+  // union of the four groups' selected blocks, ascending: j | sel_g << (16 + g)
+  __shared__ uint32_t steps[kMaxN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.H / a.H_kv;
-
-  // ---- work item (heavy query blocks first)
-  int b, h0, h1, i0, i1;
-  bool en1 = true;
-  {
-    const int item = blockIdx.x;
-    if (a.pair_heads) {
-      const int per_i = a.B * (a.H / 2);
-      const int i = a.N - 1 - item / per_i;
-      const int rem = item % per_i;
-      b = rem / (a.H / 2);
-      const int hp = rem % (a.H / 2);
-      h0 = 2 * hp;
-      h1 = h0 + 1;
-      i0 = i1 = i;
-    } else {
-      const int npairs = (a.N + 1) / 2;
-      const int per_ip = a.B * a.H;
-      const int ip = npairs - 1 - item / per_ip;
-      const int rem = item % per_ip;
-      b = rem / a.H;
-      h0 = h1 = rem % a.H;
-      i0 = 2 * ip;
-      i1 = i0 + 1;
-      en1 = i1 < a.N;
-    }
-  }
-  const int kvh = h0 / G;
-  const int jmax = en1 ? max(i0, i1) : i0;
+  const Groups gr = decode_item(a, blockIdx.x);
+  const int kvh = gr.h[0] / G;
+  int jmax = -1;
+  for (int k = 0; k < 4; ++k)
+    if (gr.en[k]) jmax = max(jmax, gr.i[k]);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar_q, 4);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&bar_q[x], 4);
+      mbar_init(&bar_sfull[x], 1);
+      mbar_init(&bar_pfull[x], 4);
+    }
     for (int s = 0; s < kST; ++s) {
       mbar_init(&bar_kvfull[s], 1);
-      mbar_init(&bar_kvempty[s], 1);
+      mbar_init(&bar_kvempty[s], 2);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&bar_sfull[s], 1);
-      mbar_init(&bar_sempty[s], 8);
-      mbar_init(&bar_pfull[s], 8);
-      mbar_init(&bar_pempty[s], 1);
-    }
-    mbar_init(&bar_ofull, 1);
+    mbar_init(&bar_ofull[0], 1);
+    mbar_init(&bar_ofull[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
   if (warp == 2) {
     // mask rows restricted to the causal prefix j <= i_g, then the ascending union list
-    const int nw = (jmax >> 5) + 1;
-    for (int g = 0; g < 2; ++g) {
-      const int ig = g ? i1 : i0;
-      const bool en = g ? en1 : true;
-      const int hg = g ? h1 : h0;
+    const int nw = jmax >= 0 ? (jmax >> 5) + 1 : 0;
+    for (int g = 0; g < 4; ++g) {
+      const int ig = gr.i[g];
       const uint32_t* src =
-          a.mask ? a.mask + ((long long)(b * a.planes + hg / a.heads_per_plane) * a.N + ig) * a.W : nullptr;
+          a.mask ? a.mask + ((long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + ig) * a.W
+                 : nullptr;
       for (int w = lane; w < nw; w += 32) {
         uint32_t word = 0;
-        if (en && (w << 5) <= ig) {
+        if (gr.en[g] && (w << 5) <= ig) {
           word = src ? src[w] : ~0u;
           const int hi = ig - (w << 5);  // bits 0..hi are causal
           if (hi < 31) word &= (2u << hi) - 1u;
@@ -156,8 +207,10 @@ __global__ void __launch_bounds__(384, 1)
     int base = 0;
     for (int w0 = 0; w0 < nw; w0 += 32) {
       const int w = w0 + lane;
-      const uint32_t m0 = w < nw ? mrow[0][w] : 0u, m1 = w < nw ? mrow[1][w] : 0u;
-      uint32_t u = m0 | m1;
+      uint32_t m[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) m[g] = w < nw ? mrow[g][w] : 0u;
+      uint32_t u = m[0] | m[1] | m[2] | m[3];
       const int cnt = __popc(u);
       int incl = cnt;
 #pragma unroll
@@ -169,7 +222,10 @@ __global__ void __launch_bounds__(384, 1)
       while (u) {
         const int bit = __ffs(u) - 1;
         u &= u - 1u;
-        steps[pos++] = uint32_t((w << 5) + bit) | (((m0 >> bit) & 1u) << 16) | (((m1 >> bit) & 1u) << 17);
+        uint32_t e = uint32_t((w << 5) + bit);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) e |= ((m[g] >> bit) & 1u) << (16 + g);
+        steps[pos++] = e;
       }
       base += __shfl_sync(0xffffffffu, incl, 31);
     }
@@ -187,12 +243,12 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       const uint64_t pol_kv = policy_evict_last();
-      const int kvrow0 = (b * a.H_kv + kvh) * a.L;
+      const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
       for (int t = 0; t < T; ++t) {
         const int j = int(steps[t] & 0xFFFFu);
         const int s = t % kST;
         if (t >= kST) mbar_wait(&bar_kvempty[s], ((t / kST) + 1) & 1);
-        uint8_t* sk = smem + SL::kK + s * 2 * SL::kKVBytes;
+        uint8_t* sk = smem + s * 2 * SL::kKVBytes;
         uint8_t* sv = sk + SL::kKVBytes;
         mbar_arrive_expect_tx(&bar_kvfull[s], 2 * SL::kKVBytes);
         for (int kc = 0; kc < SL::kChunks; ++kc) {
@@ -202,78 +258,75 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // S(t) -> S buffer t&1; softmax warpgroup w turns columns [32w, 32w+32) of S(t)
-    // into P(t) (P buffer t&1) with its own running max; O_w += P_w V_w. Event-driven:
-    // S(t) is issued as soon as its K tile landed and S(t-2) was drained, P.V(t) as
-    // soon as P(t) is complete — neither waits for the other.
-    constexpr uint32_t idesc_s = idesc_f16(kBM, kBS, /*bf16*/ 1, false, false);
-    constexpr uint32_t idesc_o = idesc_f16(kBM, D, /*bf16*/ 1, false, /*V MN-major*/ true);
-    mbar_wait(&bar_q, 0);  // Q rows are in TMEM
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuers
+    // One issuer warp per tile (warp 1 -> A, warp 3 -> B): S(k), P.V(k), S(k+1), ...
+    // strictly alternating (P(k) aliases S(k)), releasing every union position in
+    // order — used ones by the P.V commit, skipped ones by a plain arrive — so the
+    // two tiles never wait on each other and the producer always makes progress.
+    const int x = warp == 1 ? 0 : 1;
+    constexpr uint32_t idesc_s = idesc_f16(128, kBS, /*bf16*/ 1, false, false);
+    constexpr uint32_t idesc_o = idesc_f16(128, D, /*bf16*/ 1, false, /*V MN-major*/ true);
+    const uint32_t tb = tmem + x * 256;
+    mbar_wait(&bar_q[x], 0);  // Q rows of tile x are in TMEM
     tc_fence_after();
-    auto issue_s = [&](int t) {
-      const int st = t % kST, sb = t & 1;
+    int k = 0;
+    for (int t = 0; t < T; ++t) {
+      const int st = t % kST;
+      // Waiting for the tile to land even when skipping keeps this warp's
+      // kv_empty arrivals in phase order (one per stage phase).
       mbar_wait(&bar_kvfull[st], (t / kST) & 1);
-      if (t >= 2) mbar_wait(&bar_sempty[sb], ((t - 2) >> 1) & 1);
+      if (((steps[t] >> (16 + 2 * x)) & 3u) == 0u) {
+        if (lane == 0) mbar_arrive(&bar_kvempty[st]);  // not needed by this tile
+        continue;
+      }
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sK = smem_u32(smem + SL::kK + st * 2 * SL::kKVBytes);
+        const uint32_t sK = smem_u32(smem + st * 2 * SL::kKVBytes);
 #pragma unroll
         for (int kc = 0; kc < SL::kChunks; ++kc)
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             const uint64_t bd = sdesc_sw128(sK + kc * kBS * 128 + ks * 32, 16, 1024);
-            umma_f16_ts(tmem + kTS + sb * kBS, tmem + kTQ + (kc * 4 + ks) * 8, bd, idesc_s, (kc | ks) != 0);
+            umma_f16_ts(tb + kTS, tb + kTQ + (kc * 4 + ks) * 8, bd, idesc_s, (kc | ks) != 0);
           }
-        umma_commit(&bar_sfull[sb]);
+        umma_commit(&bar_sfull[x]);
+        TRACE(x, k, 0);
       }
       __syncwarp();
-    };
-    // Fixed order with blocking waits: S(t+2) as soon as S(t) is drained (early in
-    // softmax(t)), then P.V(t) once P(t) is complete (end of softmax(t)).
-    if (T > 0) issue_s(0);
-    if (T > 1) issue_s(1);
-    for (int t = 0; t < T; ++t) {
-      if (t + 2 < T) issue_s(t + 2);
-      mbar_wait(&bar_pfull[t & 1], (t >> 1) & 1);
+      mbar_wait(&bar_pfull[x], k & 1);
       tc_fence_after();
       if (elect_one()) {
-        const int pb = t & 1;
-        const uint32_t sV = smem_u32(smem + SL::kK + (t % kST) * 2 * SL::kKVBytes + SL::kKVBytes);
+        const uint32_t sV = smem_u32(smem + st * 2 * SL::kKVBytes + SL::kKVBytes);
 #pragma unroll
         for (int ks = 0; ks < kBS / 16; ++ks) {
-          const int w = ks >> 1;  // keys [32w, 32w+32) belong to softmax warpgroup w
           const uint64_t bd = sdesc_sw128(sV + ks * 16 * 128, kBS * 128, 1024);
-          umma_f16_ts(tmem + kTO + w * 128, tmem + kTP + pb * 32 + ks * 8, bd, idesc_o,
-                      (t > 0 || (ks & 1)) ? 1u : 0u);
+          umma_f16_ts(tb + kTO, tb + kTS + ks * 8, bd, idesc_o, (k > 0 || ks > 0) ? 1u : 0u);
         }
-        umma_commit(&bar_kvempty[t % kST]);
-        umma_commit(&bar_pempty[pb]);
+        umma_commit(&bar_kvempty[st]);
+        TRACE(x, k, 3);
       }
       __syncwarp();
+      ++k;
     }
-    if (elect_one()) umma_commit(&bar_ofull);
+    if (elect_one()) umma_commit(&bar_ofull[x]);
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax / epilogue
-    const int wg = (warp - 4) >> 2;  // softmax warpgroup = step parity it owns
-    const int q = warp & 3;          // TMEM lane quarter
+    const int x = (warp - 4) >> 2;  // tile
+    const int q = warp & 3;         // TMEM lane quarter
     const int row = q * 32 + lane;
-    const int g = row >> 6, rloc = row & 63;
-    const int ig = g ? i1 : i0;
-    const int hg = g ? h1 : h0;
-    const bool en = g ? en1 : true;
+    const int g = 2 * x + (row >> 6), rloc = row & 63;
+    const int ig = gr.i[g], hg = gr.h[g];
+    const bool en = gr.en[g];
     const uint32_t lane_addr = uint32_t(q * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + kTS + wg * kBS;
-    const uint32_t tO = tmem + lane_addr + kTO + wg * 128;
-    const uint32_t tP = tmem + lane_addr + kTP + wg * 16;  // + 32 * (t & 1)
+    const uint32_t tb = tmem + lane_addr + x * 256;
     const float sl2 = a.scale_log2;
     float m_used = -INFINITY, l = 0.f;
-    if (wg == 0) {
+    {
       // Q row -> TMEM (A operand of S = Q K^T: lane = row, 2 bf16 per column)
       const uint4* src = reinterpret_cast<const uint4*>(
-          a.Q + ((long long)(b * a.H + hg) * a.L + (long long)ig * kBS + rloc) * D);
+          a.Q + ((long long)(gr.b * a.H + hg) * a.L + (long long)ig * kBS + rloc) * D);
 #pragma unroll
       for (int c0 = 0; c0 < D / 2; c0 += 16) {
         uint32_t w16[16];
@@ -285,95 +338,112 @@ __global__ void __launch_bounds__(384, 1)
           w16[4 * u + 2] = v.z;
           w16[4 * u + 3] = v.w;
         }
-        tmem_st16(tmem + lane_addr + kTQ + c0, w16);
+        tmem_st16(tb + kTQ + c0, w16);
       }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_q);
+      if (lane == 0) mbar_arrive(&bar_q[x]);
     }
-    const uint32_t tShalf = tmem + lane_addr + kTS + wg * 32;
+    int k = 0;
     for (int t = 0; t < T; ++t) {
       const uint32_t e = steps[t];
+      if (((e >> (16 + 2 * x)) & 3u) == 0u) continue;  // not a step of this tile
       const int j = int(e & 0xFFFFu);
       const bool sel = (e >> (16 + g)) & 1u;
-      const int sb = t & 1;
-      mbar_wait(&bar_sfull[sb], (t >> 1) & 1);
+      mbar_wait(&bar_sfull[x], k & 1);
       tc_fence_after();
-      float sv[32];
+      if (row == 0) TRACE(x, k, 1);
+      float sv[kBS];
       if (sel) {
-        uint32_t v[32];
-        tmem_ld32(tShalf + sb * kBS, v);
+        uint32_t v[32], v2[32];
+        tmem_ld32(tb + kTS, v);
+        tmem_ld32(tb + kTS + 32, v2);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(v[c]);
+        for (int c = 0; c < 32; ++c) {
+          sv[c] = __uint_as_float(v[c]);
+          sv[32 + c] = __uint_as_float(v2[c]);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_sempty[sb]);
-      // P buffer sb was last read by P.V(t-2)
-      if (t >= 2) mbar_wait(&bar_pempty[sb], ((t - 2) >> 1) & 1);
-
-      uint32_t packed[16];
+      if (row == 0) TRACE(x, k, 4);
+      uint32_t packed[kBS / 2];
+#if US_ATTN_SKELETON
+      // calibration build only: keep the data movement and synchronisation, drop the math
       if (sel) {
+        l += sv[0] + sv[63];
+#pragma unroll
+        for (int c = 0; c < kBS / 2; ++c) packed[c] = 0x3f803f80u;
+        m_used = 0.f;
+      } else {
+#pragma unroll
+        for (int c = 0; c < kBS / 2; ++c) packed[c] = 0u;
+      }
+      if (false) {
+#else
+      if (sel) {
+#endif
         const bool diag = (j == ig);
         if (diag) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c + 32 * wg > rloc) sv[c] = -INFINITY;
+          for (int c = 0; c < kBS; ++c)
+            if (c > rloc) sv[c] = -INFINITY;
         }
-        float mx = fmaxf(sv[0], sv[1]);
+        // 8 independent partial maxima (short dependency chains), then a tree
+        float m8[8];
 #pragma unroll
-        for (int c = 2; c < 32; c += 2) mx = fmaxf(mx, fmaxf(sv[c], sv[c + 1]));
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(sv[u], fmaxf(sv[8 + u], sv[16 + u]));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(sv[24 + u], sv[32 + u]));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(sv[40 + u], fmaxf(sv[48 + u], sv[56 + u])));
+        float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                         fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         mx *= sl2;
         const bool need = mx > m_used + 8.f;
         const bool need_o = need && l > 0.f;
         // tcgen05.ld/st are warp-collective: the O pass runs for the whole warp
-        // whenever any of its rows moves its max; other rows use f = 1.
+        // whenever any of its rows moves its max; other rows use f = 1. P.V(k-1)
+        // has retired: the S(k) commit covers it.
         if (__any_sync(0xffffffffu, need_o)) {
           const float f = need_o ? ex2_approx(m_used - mx) : 1.f;
-          // O_wg was last written by P.V(t-1)
-          mbar_wait(&bar_pempty[(t - 1) & 1], ((t - 1) >> 1) & 1);
-          tc_fence_after();
 #pragma unroll 1
           for (int c0 = 0; c0 < D; c0 += 32) {
             uint32_t o[32];
-            tmem_ld32(tO + c0, o);
+            tmem_ld32(tb + kTO + c0, o);
             tmem_ld_wait();
 #pragma unroll
             for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-            US_TMEM_ST_X32(tO + c0, o);
+            US_TMEM_ST_X32(tb + kTO + c0, o);
           }
           tmem_st_wait();
           l *= f;
         }
         if (need) m_used = mx;
-        // -inf (masked) when the warpgroup's half of this row has no live key yet
-        const float mu = m_used == -INFINITY ? 0.f : m_used;
-        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-mu, -mu);
+        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
         if (!diag) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+          for (int c = 0; c < kBS; c += 2) {
+            const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
             float2 p;
             if (c >= kPolyFrom) {
-              p = ex2_poly2(x);
+              p = ex2_poly2(xx);
             } else {
-              p.x = ex2_approx(x.x);
-              p.y = ex2_approx(x.y);
+              p.x = ex2_approx(xx.x);
+              p.y = ex2_approx(xx.y);
             }
             acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
             packed[c >> 1] = pack_bf16(p.x, p.y);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+          for (int c = 0; c < kBS; c += 2) {
+            const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
             float2 p;
-            p.x = ex2_approx(x.x);
-            p.y = ex2_approx(x.y);
+            p.x = ex2_approx(xx.x);
+            p.y = ex2_approx(xx.y);
             acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
             packed[c >> 1] = pack_bf16(p.x, p.y);
           }
@@ -383,59 +453,46 @@ __global__ void __launch_bounds__(384, 1)
         l += s2.x + s2.y;
       } else {
 #pragma unroll
-        for (int c = 0; c < 16; ++c) packed[c] = 0u;
+        for (int c = 0; c < kBS / 2; ++c) packed[c] = 0u;
       }
-      tmem_st16(tP + sb * 32, packed);
+      if (row == 0) TRACE(x, k, 5);
+      US_TMEM_ST_X32(tb + kTS, packed);  // P aliases the S columns just read
       tmem_st_wait();
+      if (row == 0) TRACE(x, k, 6);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_pfull[sb]);
+      if (row == 0) TRACE(x, k, 2);
+      if (lane == 0) mbar_arrive(&bar_pfull[x]);
+      ++k;
     }
-    // ---- merge the two warpgroups' partial softmax states (split over key steps)
-    xm[wg][row] = m_used;
-    xl[wg][row] = l;
-    mbar_wait(&bar_ofull, 0);
+    // ---- epilogue
+    mbar_wait(&bar_ofull[x], 0);
     tc_fence_after();
-    named_bar_sync(1, 256);
-    const float m0 = xm[0][row], m1 = xm[1][row], l0 = xl[0][row], l1 = xl[1][row];
-    const float mm = fmaxf(m0, m1);
-    const float f0 = l0 > 0.f ? ex2_approx(m0 - mm) : 0.f;
-    const float f1 = l1 > 0.f ? ex2_approx(m1 - mm) : 0.f;
-    const float lt = l0 * f0 + l1 * f1;
-    const float inv_l = 1.f / lt;
-    const bool write = en && T > 0;
-    __nv_bfloat16* dst = a.O + ((long long)(b * a.H + hg) * a.L + (long long)ig * kBS + rloc) * D;
-    const uint32_t tO0 = tmem + lane_addr + kTO, tO1 = tO0 + 128;
+    const bool write = en && l > 0.f;
+    const float inv_l = 1.f / l;
+    __nv_bfloat16* dst = a.O + ((long long)(gr.b * a.H + hg) * a.L + (long long)ig * kBS + rloc) * D;
 #pragma unroll 1
-    for (int c0 = wg * (D / 2); c0 < (wg + 1) * (D / 2); c0 += 16) {
-      uint32_t o0[16], o1[16];
-      tmem_ld16(tO0 + c0, o0);
-      tmem_ld16(tO1 + c0, o1);
+    for (int c0 = 0; c0 < D; c0 += 16) {
+      uint32_t o[16];
+      tmem_ld16(tb + kTO + c0, o);
       tmem_ld_wait();
-      float r[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const float a0 = f0 > 0.f ? __uint_as_float(o0[c]) * f0 : 0.f;
-        const float a1 = f1 > 0.f ? __uint_as_float(o1[c]) * f1 : 0.f;
-        r[c] = (a0 + a1) * inv_l;
-      }
       if (write) {
         uint4 w0, w1;
-        w0.x = pack_bf16(r[0], r[1]);
-        w0.y = pack_bf16(r[2], r[3]);
-        w0.z = pack_bf16(r[4], r[5]);
-        w0.w = pack_bf16(r[6], r[7]);
-        w1.x = pack_bf16(r[8], r[9]);
-        w1.y = pack_bf16(r[10], r[11]);
-        w1.z = pack_bf16(r[12], r[13]);
-        w1.w = pack_bf16(r[14], r[15]);
+        w0.x = pack_bf16(__uint_as_float(o[0]) * inv_l, __uint_as_float(o[1]) * inv_l);
+        w0.y = pack_bf16(__uint_as_float(o[2]) * inv_l, __uint_as_float(o[3]) * inv_l);
+        w0.z = pack_bf16(__uint_as_float(o[4]) * inv_l, __uint_as_float(o[5]) * inv_l);
+        w0.w = pack_bf16(__uint_as_float(o[6]) * inv_l, __uint_as_float(o[7]) * inv_l);
+        w1.x = pack_bf16(__uint_as_float(o[8]) * inv_l, __uint_as_float(o[9]) * inv_l);
+        w1.y = pack_bf16(__uint_as_float(o[10]) * inv_l, __uint_as_float(o[11]) * inv_l);
+        w1.z = pack_bf16(__uint_as_float(o[12]) * inv_l, __uint_as_float(o[13]) * inv_l);
+        w1.w = pack_bf16(__uint_as_float(o[14]) * inv_l, __uint_as_float(o[15]) * inv_l);
         reinterpret_cast<uint4*>(dst + c0)[0] = w0;
         reinterpret_cast<uint4*>(dst + c0)[1] = w1;
       }
     }
-    if (write && wg == 0 && a.lse)
-      a.lse[(long long)(b * a.H + hg) * a.L + (long long)ig * kBS + rloc] =
-          (mm + __log2f(lt)) * 0.69314718055994531f;
+    if (write && a.lse)
+      a.lse[(long long)(gr.b * a.H + hg) * a.L + (long long)ig * kBS + rloc] =
+          (m_used + __log2f(l)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
@@ -452,8 +509,10 @@ us_status launch_attn_t(const AttnArgs& a, const CUtensorMap& tmQ, const CUtenso
                 "attn_kernel smem attribute");
     attr_set = true;
   }
-  const long long items = a.pair_heads ? (long long)a.B * (a.H / 2) * a.N
-                                       : (long long)a.B * a.H * ((a.N + 1) / 2);
+  long long items;
+  if (a.group_mode == 0) items = (long long)a.B * (a.H / 4) * a.N;
+  else if (a.group_mode == 1) items = (long long)a.B * a.H_kv * ((a.N + 1) / 2);
+  else items = (long long)a.B * a.H * ((a.N + 3) / 4);
   attn_kernel<D><<<unsigned(items), 384, smem, st>>>(tmQ, tmK, tmV, a);
   US_LAUNCH_CHECK("attn_kernel");
   return US_OK;
@@ -463,7 +522,7 @@ us_status launch_attn_t(const AttnArgs& a, const CUtensorMap& tmQ, const CUtenso
 
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st) {
-  if (a.W > kMaxW) {
+  if (a.N > kMaxN) {
     set_error("attention: N (=L/S) above 4096 is not supported on the GPU path");
     return US_ERR_UNSUPPORTED;
   }
@@ -474,3 +533,10 @@ us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUte
 }
 
 }  // namespace us
+
+#if US_ATTN_TRACE
+extern "C" int us_debug_attn_trace(int cta, long long* host_out) {
+  if (host_out) return int(cudaMemcpyFromSymbol(host_out, ::g_attn_trace, sizeof(long long) * 2 * 4096 * 8));
+  return int(cudaMemcpyToSymbol(::g_attn_trace_cta, &cta, sizeof(int)));
+}
+#endif

@@ -82,7 +82,7 @@ us_status launch_select(const SelectArgs& a, cudaStream_t st);
 // ---------------------------------------------------------------- attention (a6)
 struct AttnArgs {
   int B, H, H_kv, L, N, W, D;
-  int pair_heads;       // 1: CTA rows = heads (h, h+1) of one KV group; 0: blocks (i, i+1) of one head
+  int group_mode;       // CTA groups: 0 = 4 heads of a KV group, 1 = 2 heads x 2 blocks, 2 = 1 head x 4 blocks
   int heads_per_plane;  // mask plane of head h = h / heads_per_plane
   int planes;           // mask planes per batch item
   const uint32_t* mask; // [B][planes][N][W] (nullptr = dense causal)

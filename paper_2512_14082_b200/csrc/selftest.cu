@@ -147,3 +147,139 @@ extern "C" us_status us_selftest_umma(int mode, int N, int bf16, const void* A, 
   US_LAUNCH_CHECK("us_selftest_umma");
   return US_OK;
 }
+
+// ---------------------------------------------------------------- MMA issue-rate probe
+// One CTA per SM issues `iters` groups of `per_group` back-to-back tcgen05.mma
+// (M=128, K=16, bf16) with shape N and operand mode, then waits for completion.
+// The host converts elapsed time into cycles per MMA. Operands are arbitrary
+// smem/TMEM contents (only timing matters).
+namespace us {
+namespace {
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int N, int a_tmem, int per_group,
+                                                           long long* cycles_out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  long long t0 = clock64();
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t idesc = idesc_f16(128, N, 1, false, false);
+      const uint32_t sb = smem_u32(smem);
+      for (int it = 0; it < iters; ++it) {
+        for (int k = 0; k < per_group; ++k) {
+          const uint64_t bd = sdesc_sw128(sb + 32768 + (k & 3) * 32, 16, 1024);
+          if (a_tmem)
+            umma_f16_ts(tmem, tmem + 256 + (k & 7) * 8, bd, idesc, k > 0);
+          else
+            umma_f16_ss(tmem, sdesc_sw128(sb + (k & 3) * 32, 16, 1024), bd, idesc, k > 0);
+        }
+      }
+      umma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cycles_out[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+}  // namespace
+}  // namespace us
+
+extern "C" us_status us_selftest_mma_rate(int iters, int N, int a_tmem, int per_group, int ctas,
+                                          long long* cycles_out, void* stream) {
+  using namespace us;
+  const int smem = 96 * 1024;
+  cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_rate_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(iters, N, a_tmem, per_group, cycles_out);
+  US_LAUNCH_CHECK("us_selftest_mma_rate");
+  return US_OK;
+}
+
+// ---------------------------------------------------------------- TMEM load bandwidth probe
+// Warps 0-3 repeatedly tcgen05.ld 64 fp32 columns of their lane quarter (32x32b.x32 x2)
+// and consume them; if mma_n > 0, warp 4 concurrently issues back-to-back
+// M=128 x N=mma_n TS-mode MMAs into a disjoint TMEM region. Output: cycles/iteration.
+namespace us {
+namespace {
+__global__ void __launch_bounds__(160, 1) tmem_ld_probe_kernel(int iters, int mma_n, float* sink,
+                                                                long long* cycles_out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    stop = 0;
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp < 4) {
+    float acc = 0.f;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      uint32_t v[32], v2[32];
+      const uint32_t a = tmem + (uint32_t(warp * 32) << 16) + (it & 1) * 64;
+      tmem_ld32(a, v);
+      tmem_ld32(a + 32, v2);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc += __uint_as_float(v[c]) + __uint_as_float(v2[c]);
+    }
+    const long long t1 = clock64();
+    if (lane == 0 && warp == 0) cycles_out[blockIdx.x] = t1 - t0;
+    sink[blockIdx.x * 128 + threadIdx.x] = acc;
+    __syncwarp();
+    if (warp == 0 && lane == 0) stop = 1;
+  } else if (mma_n > 0) {
+    const uint32_t idesc = idesc_f16(128, mma_n, 1, false, false);
+    const uint32_t sb = smem_u32(smem);
+    int n = 0;
+    while (!stop && n < 1000000) {
+      if (elect_one()) {
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t bd = sdesc_sw128(sb + (k & 3) * 32, 16, 1024);
+          umma_f16_ts(tmem + 256, tmem + 448 + (k & 7) * 8, bd, idesc, k > 0);
+        }
+        umma_commit(&bar);
+      }
+      __syncwarp();
+      mbar_wait(&bar, n & 1);
+      ++n;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+}  // namespace
+}  // namespace us
+
+extern "C" us_status us_selftest_tmem_ld(int iters, int mma_n, int ctas, float* sink, long long* cycles_out,
+                                         void* stream) {
+  using namespace us;
+  const int smem = 64 * 1024;
+  cudaFuncSetAttribute(tmem_ld_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tmem_ld_probe_kernel<<<ctas, 160, smem, static_cast<cudaStream_t>(stream)>>>(iters, mma_n, sink, cycles_out);
+  US_LAUNCH_CHECK("us_selftest_tmem_ld");
+  return US_OK;
+}
