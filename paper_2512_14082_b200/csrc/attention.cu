@@ -99,6 +99,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 
 constexpr int kPolyFrom = 48;  // columns [48, 64) of an off-diagonal tile use ex2_poly2 (25%)
 
+// Work order: KV head outermost, query blocks heaviest-first inside it, so the
+// ~148 resident CTAs all stream K/V of ONE KV head (L * d * 4 bytes = 64 MB at
+// 128K, d=128) and their random selected-block reads hit the 126 MB L2. The
+// earlier query-block-major order spread them over every KV head (the whole
+// 512 MB K/V) and ncu measured 130 GB of DRAM reads per layer (r01 profile).
 struct Groups {
   int b, h[4], i[4];
   bool en[4];
@@ -109,11 +114,10 @@ __device__ __forceinline__ Groups decode_item(const AttnArgs& a, int item) {
   const int G = a.H / a.H_kv;
   if (a.group_mode == 0) {  // 4 heads of a KV group, one query block
     const int quads = a.H / 4;
-    const int per_i = a.B * quads;
-    const int i = a.N - 1 - item / per_i;
-    const int rem = item % per_i;
-    g.b = rem / quads;
-    const int h0 = (rem % quads) * 4;
+    const int i = a.N - 1 - item % a.N;
+    const int bq = item / a.N;
+    g.b = bq / quads;
+    const int h0 = (bq % quads) * 4;
     for (int k = 0; k < 4; ++k) {
       g.h[k] = h0 + k;
       g.i[k] = i;
@@ -121,11 +125,10 @@ __device__ __forceinline__ Groups decode_item(const AttnArgs& a, int item) {
     }
   } else if (a.group_mode == 1) {  // 2 heads x query blocks (i, i-1)
     const int npairs = (a.N + 1) / 2;
-    const int per_ip = a.B * a.H_kv;
-    const int ip = npairs - 1 - item / per_ip;
-    const int rem = item % per_ip;
-    g.b = rem / a.H_kv;
-    const int h0 = (rem % a.H_kv) * G;
+    const int ip = npairs - 1 - item % npairs;
+    const int bk = item / npairs;
+    g.b = bk / a.H_kv;
+    const int h0 = (bk % a.H_kv) * G;
     const int ib = 2 * ip + 1, ia = 2 * ip;
     for (int k = 0; k < 4; ++k) {
       g.h[k] = h0 + (k & 1);
@@ -134,12 +137,11 @@ __device__ __forceinline__ Groups decode_item(const AttnArgs& a, int item) {
     for (int k = 0; k < 4; ++k) g.en[k] = g.i[k] < a.N;
   } else {  // one head, 4 query blocks
     const int nq = (a.N + 3) / 4;
-    const int per_q = a.B * a.H;
-    const int iq = nq - 1 - item / per_q;
-    const int rem = item % per_q;
-    g.b = rem / a.H;
+    const int iq = nq - 1 - item % nq;
+    const int bh = item / nq;
+    g.b = bh / a.H;
     for (int k = 0; k < 4; ++k) {
-      g.h[k] = rem % a.H;
+      g.h[k] = bh % a.H;
       g.i[k] = 4 * iq + 3 - k;
       g.en[k] = g.i[k] < a.N;
     }
