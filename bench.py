@@ -186,7 +186,7 @@ def main():
               "head_dim": d, "block": 64, "c_q": 8, "c_k": 8, "c_h": 1,
               "selection": f"top_p P={P}" if mode == "top_p" else f"top_k k={sel}",
               "causal_mode": "post-softmax-block-causal", "batch": 1,
-              "parallelism": f"head-partitioned x{args.gpus} (KV groups per rank)",
+              "parallelism": f"head-partitioned x{world} (paper_2512_14082_b200/shard.py; no hot-path collective)",
               "l2": "inputs (>=192 MB per rank) exceed the 126 MB L2; no flush needed"}
 
     if args.impl == "reference":
@@ -215,11 +215,11 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
-    if H_kv % world != 0:
-        raise SystemExit(f"H_kv={H_kv} not divisible by {world} GPUs")
-    kv_per = H_kv // world
+    from paper_2512_14082_b200.shard import gather_heads, imbalance, shard_heads
+    shards = shard_heads(H, H_kv, world)
+    shard = shards[rank]
     G = H // H_kv
-    heads = list(range(rank * kv_per * G, (rank + 1) * kv_per * G))
+    heads = list(shard.q_heads)
     Q, K, V = workloads.planted_blocks(L, H, H_kv, d, 64, seed=args.seed, gain=gain, heads=heads)
     torch.cuda.synchronize()
     cfg = us.CompressionConfig(P=P) if mode == "top_p" else us.CompressionConfig(
@@ -291,6 +291,18 @@ def main():
     h2d = (Q.numel() + K.numel() + V.numel()) * 2 * world
     d2h = Q.numel() * 2 * world
 
+    # ---------------------------------------------------------------- NCCL gather (verification only, untimed)
+    gather = None
+    if dist:
+        t0 = time.perf_counter()
+        full = gather_heads(eng.O, shards)
+        torch.cuda.synchronize()
+        sl = full[:, shard.q_heads.start:shard.q_heads.stop]
+        gather = {"backend": dist.get_backend(), "ok": bool(torch.equal(sl, eng.O)),
+                  "bytes": full.numel() * full.element_size(), "s": time.perf_counter() - t0,
+                  "head_imbalance": imbalance(shards)}
+        del full, sl
+
     # ---------------------------------------------------------------- dense baselines (same shard)
     dense = {}
     if not args.no_dense:
@@ -342,7 +354,7 @@ def main():
     if os.path.exists(tp):
         roof["traffic"] = json.load(open(tp)).get(args.config, {}).get(roof["kernel"].split()[0])
     roof["peak_source"] = f"MEASURED_PEAKS.json ({peak_src}, sustained bf16)"
-    comp_bytes = (len(heads) + len(heads) // G) * L * d * 2 + (len(heads) + len(heads) // G) * (L // 8) * d * 4
+    comp_bytes = (len(heads) + shard.H_kv) * L * d * 2 + (len(heads) + shard.H_kv) * (L // 8) * d * 4
     stage_roofs = {
         "compress": {"bound": "hbm", "bytes": comp_bytes,
                      "achieved_gbs": comp_bytes / (stage_ms["compress"] * 1e-3) / 1e9, "peak_gbs": hbm},
@@ -364,7 +376,7 @@ def main():
                roofline=roof, cpu_baseline=cpu,
                stages_ms=stage_ms, stage_roofline=stage_roofs,
                sparsity={"rho": rho, "selected_blocks": selected, "causal_blocks": causal},
-               dense_baselines_ms=dense,
+               dense_baselines_ms=dense, verify_gather=gather,
                speedup_vs_dense={"vs": fastest[0], "dense_ms": fastest[1], "speedup": fastest[1] / ms} if fastest else None)
     print(json.dumps(out), flush=True)
     if dist:

@@ -106,6 +106,13 @@ const char* us_last_error(void);
  * number of violations; msg receives them joined by "; ". */
 int us_validate(const us_params* p, char* msg, size_t cap);
 
+/* The host-side gate every call below runs first, exposed so wrappers can
+ * raise before allocating: US_OK, US_ERR_INVALID_ARGUMENT (reference
+ * validate_inputs violations, text "<who>: v1; v2", types.cpp:97-123) or
+ * US_ERR_UNSUPPORTED (GPU-path limits); message via us_last_error().
+ * need_compression = 0 skips the compression-only limits (attention calls). */
+us_status us_check_params(const us_params* p, const char* who, int32_t need_compression);
+
 /* Device workspace needed by any call below for these params. */
 size_t us_workspace_bytes(const us_params* p);
 

@@ -54,7 +54,30 @@ def build(verbose: bool = False, force: bool = False) -> str:
         list(ex.map(run, jobs))
     if force or jobs or not _newer(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda" if False else "-lrt"])
+    build_wrapper_test(force)
     return LIB
+
+
+WRAPPER_SRC = os.path.join(os.path.dirname(PKG), "tests", "cpp", "wrapper_test.cpp")
+WRAPPER_BIN = os.path.join(OUT_DIR, "wrapper_test")
+
+
+def build_wrapper_test(force: bool = False) -> str:
+    """C++ test of the header-only reference-API mirror (include/unisparse_b200.hpp),
+    linked against the in-tree library (rpath $ORIGIN)."""
+    inc = os.path.join(os.path.dirname(PKG), "include")
+    deps = [WRAPPER_SRC, LIB, os.path.join(inc, "unisparse_b200.hpp"), os.path.join(inc, "us_api.h")]
+    if not force and _newer(WRAPPER_BIN, deps):
+        return WRAPPER_BIN
+    cuda = os.path.dirname(os.path.dirname(os.path.realpath(NVCC)))
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    cmd = [cxx, "-O2", "-std=c++17", "-Wall", f"-I{inc}", f"-I{cuda}/include", WRAPPER_SRC, "-o", WRAPPER_BIN,
+           f"-L{OUT_DIR}", "-lunisparse_b200", f"-L{cuda}/lib64", "-lcudart", "-Wl,-rpath,$ORIGIN",
+           f"-Wl,-rpath,{cuda}/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"g++ failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return WRAPPER_BIN
 
 
 if __name__ == "__main__":

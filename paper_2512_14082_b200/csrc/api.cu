@@ -380,6 +380,10 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
   return int(all.size());
 }
 
+us_status us_check_params(const us_params* p, const char* who, int32_t need_compression) {
+  return gate(p, who ? who : "us_check_params", need_compression != 0);
+}
+
 size_t us_workspace_bytes(const us_params* p) {
   if (!p || !check(*p, false).errors.empty()) return 0;
   return layout(*p).total;
@@ -473,7 +477,8 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
 us_status us_unisparse_attention(const us_params* p, const void* Q, const void* K, const void* V,
                                  void* O, float* lse, const us_selection* sel, void* workspace,
                                  size_t workspace_bytes, void* stream) {
-  us_status s = gate(p, "unisparse_attn", true);
+  // unisparse_attn validates through select_blocks (pipeline.cpp:19-24 -> :7-8)
+  us_status s = gate(p, "select_blocks", true);
   if (s != US_OK) return s;
   if ((s = need_ws(*p, workspace, workspace_bytes, "unisparse_attn")) != US_OK) return s;
   Geo g(*p);
