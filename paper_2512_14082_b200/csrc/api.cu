@@ -148,7 +148,7 @@ struct Geo {
 
 struct Ws {
   size_t err, first_bad, fb_count, absmax_q, absmax_k, exp_q, exp_k, fb_rows, qc, kc, qh, ql, kh,
-      kl, lse2, scores, mask, total;
+      kl, lse2, part, tmax, scores, mask, total;
   size_t header_bytes;  // [0, header_bytes) is cleared before each selection
 };
 
@@ -183,6 +183,11 @@ Ws layout(const us_params& p) {
   w.kh = take(2 * krows * g.D);
   w.kl = take(2 * krows * g.D);
   w.lse2 = take(4 * qplanes * g.Lq);
+  // slot partials of the one-pass proxy: [qplanes][T][Lq][128/sw] (= Lq * Lk/sw per plane)
+  const size_t T = (size_t(g.Lk) + 127) / 128;
+  const size_t ns = 128 / size_t(proxy_slot_width(g.rk));
+  w.part = take(4 * qplanes * T * g.Lq * ns);
+  w.tmax = take(4 * qplanes * T * g.Lq);
   w.scores = take(4 * rows * g.N);
   w.mask = take(4 * rows * g.W);
   w.total = o;
@@ -226,10 +231,8 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   if ((s = launch_split(sk, st)) != US_OK) return s;
 
   g_prof.mark(prof_call, 1, st);
-  const uint64_t qrows = uint64_t(g.B) * g.Hc * g.Lq + 128, krows = uint64_t(g.B) * g.kv_planes * g.Lk + 128;
-  CUtensorMap tQh, tQl, tKh, tKl;
-  if ((s = make_tmap_2d_16b(&tQh, at<void>(ws, w.qh), qrows, g.D, 128, 64, false)) != US_OK) return s;
-  if ((s = make_tmap_2d_16b(&tQl, at<void>(ws, w.ql), qrows, g.D, 128, 64, false)) != US_OK) return s;
+  const uint64_t krows = uint64_t(g.B) * g.kv_planes * g.Lk + 128;
+  CUtensorMap tKh, tKl;
   if ((s = make_tmap_2d_16b(&tKh, at<void>(ws, w.kh), krows, g.D, 128, 64, false)) != US_OK) return s;
   if ((s = make_tmap_2d_16b(&tKl, at<void>(ws, w.kl), krows, g.D, 128, 64, false)) != US_OK) return s;
   ProxyArgs pa{};
@@ -249,11 +252,16 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   pa.kv_div = g.kv_div;
   pa.exp_q = at<int>(ws, w.exp_q);
   pa.exp_k = at<int>(ws, w.exp_k);
+  pa.qh = at<__half>(ws, w.qh);
+  pa.ql = at<__half>(ws, w.ql);
+  pa.T = (g.Lk + 127) / 128;
+  pa.sw = proxy_slot_width(g.rk);
+  pa.part = at<float>(ws, w.part);
+  pa.tmax = at<float>(ws, w.tmax);
   pa.lse2 = at<float>(ws, w.lse2);
   pa.scores = at<float>(ws, w.scores);
   pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
-  if ((s = launch_proxy(pa, tQh, tQl, tKh, tKl, 1, st)) != US_OK) return s;
-  return launch_proxy(pa, tQh, tQl, tKh, tKl, 2, st);
+  return launch_proxy(pa, tKh, tKl, st);
 }
 
 us_status run_select_rows(const us_params& p, const float* scores, int planes, uint32_t* mask,

@@ -52,14 +52,19 @@ struct ProxyArgs {
   int kv_mul, kv_div;  // K plane of compressed head hc = hc * kv_mul / kv_div
   const int* exp_q;    // [B*Hc]
   const int* exp_k;    // [B*kv_planes]
-  float* lse2;         // [B][Hc][Lq] row log-sum-exp in log2 units (pass 1 out, pass 2 in)
-  float* scores;       // [B][Hc][N][N] block scores (pass 2 out; j <= i)
+  const __half* qh;    // [B*Hc][Lq][D] fp16 hi of Qc * 2^e
+  const __half* ql;    // [B*Hc][Lq][D] fp16 lo
+  int T;               // key tiles of 128 composite keys = ceil(Lk / 128)
+  int sw;              // slot width in composite keys = min(rk, 8)
+  float* part;         // [B*Hc][T][Lq][128/sw] slot sums of 2^(x - tile max)
+  float* tmax;         // [B*Hc][T][Lq] tile max (log2 units)
+  float* lse2;         // [B*Hc][Lq] row log-sum-exp in log2 units
+  float* scores;       // [B*Hc][N][N] block scores (j <= i)
   float scale_log2;    // log2(e) / sqrt(d_k)
 };
-// pass 1: per composite row lse over all (post) or live (pre) keys.
-// pass 2: per (query block, key block <= i) region sums of exp2(x - lse2).
-us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmQh, const CUtensorMap& tmQl,
-                       const CUtensorMap& tmKh, const CUtensorMap& tmKl, int pass,
+int proxy_slot_width(int rk);
+// One pass (logits, row LSE, slot partials) then the finalize (block scores).
+us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl,
                        cudaStream_t st);
 
 // ---------------------------------------------------------------- selection (a4-a5)

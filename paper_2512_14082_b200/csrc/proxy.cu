@@ -10,21 +10,30 @@
 // hi = fp16(x 2^e), lo = fp16(x 2^e - hi) (~22 significant bits). Each logit
 // tile is accumulated by three tcgen05 MMAs into one fp32 TMEM accumulator:
 // hi.hi + hi.lo + lo.hi (the dropped lo.lo term is < 2^-22 relative). This is
-// fp32-class accuracy at bf16 tensor-core rate — plain bf16/tf32 composite
+// fp32-class accuracy at f16 tensor-core rate — plain bf16/tf32 composite
 // tokens flip mask bits vs the fp64 reference.
 //
-// Work split (the row LSE needs every key before any score can be formed):
-//   pass 1: CTA = 128 composite query rows; streams all key tiles (post) or the
-//           live ones (pre); online max/sum in log2 units -> lse2[row].
-//   pass 2: same CTA tiling over causal key tiles only; p = 2^(x - lse2),
-//           region sums over rk keys (thread-local) and rq rows (warp shuffles,
-//           fixed tree) -> scores[i][j], j <= i.
+// ONE pass over the logits. Post-softmax needs each row's LSE over every key
+// before any probability is known, so instead of recomputing the causal half
+// (a second MMA pass), each row keeps, per causal key tile t, the tile max
+// m_t and the slot sums P_t[s] = sum_{keys in slot s} 2^(x - m_t) (a slot is
+// SW = min(rk, 8) consecutive composite keys, so every key block is a whole
+// number of slots), written to HBM; the row LSE accumulates online. The
+// finalize kernel then forms
+//     score(i, j) = sum_{rows r of block i} 2^(m_t(r) - lse2(r)) * sum_{slots of j} P_t(r)[s]
+// in a fixed order. Cost: 1x the full-square MMA work (was 1.5x) plus
+// Lq * N * 4 bytes of slot partials per plane written and read once.
 //
-// Roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (+TMEM owner),
-// warps 2..5 epilogue; epilogue warp w owns TMEM lanes 32*(w%4).. (row = lane).
-// Pipelines: K tiles double-buffered in smem (k_full/k_empty), S accumulators
-// double-buffered in TMEM (s_full/s_empty) so tile t+1's MMAs overlap tile t's
-// exp work.
+// CTA = 128 composite query rows (UMMA M = 128) of one compressed head; key
+// tiles of 128 composite keys (N = 128). Q hi/lo live in TMEM (TS-mode MMAs:
+// the A operand is read from TMEM, which measured 71.5 vs 96.3 cycles per
+// M=128/N=128/K=16 MMA against SMEM A, profiles/r01_summary.md); only K tiles
+// are streamed through SMEM by TMA.
+// Roles (320 threads): warp 0 TMA producer (K ring), warp 1 MMA issuer + TMEM
+// owner, warps 2-5 epilogue group 0 (even tiles, S buffer 0), warps 6-9
+// epilogue group 1 (odd tiles, S buffer 1). Epilogue warp w owns TMEM lanes
+// 32 * (w % 4) (thread = composite row); the two groups keep independent
+// online (max, sum) per row and merge them at the end.
 #include "host_util.hpp"
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -34,16 +43,15 @@ namespace {
 
 constexpr int kRows = 128;  // composite query rows per CTA (UMMA M)
 constexpr int kKeys = 128;  // composite keys per tile (UMMA N)
-constexpr int kStages = 2;
+// TMEM columns: S buffers [0,128) and [128,256); Q hi at 256, Q lo at 320 (D/2 cols each).
+constexpr uint32_t kTS0 = 0, kTQh = 256, kTQl = 320;
 
 template <int D>
 struct ProxySmem {
-  static constexpr int kChunks = D / 64;                 // 128-byte swizzle atoms along d
-  static constexpr int kQBytes = kRows * D * 2;          // one of hi/lo
-  static constexpr int kKBytes = kKeys * D * 2;          // one of hi/lo
-  static constexpr int kQOff = 0;                        // Qh, Ql
-  static constexpr int kKOff = 2 * kQBytes;              // stage s: Kh, Kl
-  static constexpr int kBytes = kKOff + kStages * 2 * kKBytes;
+  static constexpr int kChunks = D / 64;          // 128-byte swizzle atoms along d
+  static constexpr int kKBytes = kKeys * D * 2;   // one of hi / lo
+  static constexpr int kStages = D == 128 ? 3 : 6;
+  static constexpr int kBytes = kStages * 2 * kKBytes;
 };
 
 __device__ __forceinline__ int live_keys(int t, int c_q, int c_k, int Lk, int mode) {
@@ -53,40 +61,36 @@ __device__ __forceinline__ int live_keys(int t, int c_q, int c_k, int Lk, int mo
   return live < Lk ? int(live) : Lk;
 }
 
-template <int D, int PASS>
-__global__ void __launch_bounds__(192, 1)
-    proxy_kernel(const __grid_constant__ CUtensorMap tmQh, const __grid_constant__ CUtensorMap tmQl,
-                 const __grid_constant__ CUtensorMap tmKh, const __grid_constant__ CUtensorMap tmKl,
+template <int D, int SW>
+__global__ void __launch_bounds__(320, 1)
+    proxy_kernel(const __grid_constant__ CUtensorMap tmKh, const __grid_constant__ CUtensorMap tmKl,
                  const ProxyArgs a) {
   using L = ProxySmem<D>;
+  constexpr int kST = L::kStages;
+  constexpr int NS = kKeys / SW;  // slots per key tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q, bar_kfull[kStages], bar_kempty[kStages], bar_sfull[2], bar_sempty[2];
+  __shared__ uint64_t bar_q, bar_kfull[kST], bar_kempty[kST], bar_sfull[2], bar_sempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ float red[kRows][33];  // pass 2: per-row key-group partials of one segment
+  __shared__ float2 ml_sh[kRows];
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int rt = gridDim.x - 1 - blockIdx.x;  // heavy (late) row tiles first
+  const int rt = gridDim.x - 1 - blockIdx.x;
   const int hc = blockIdx.y, b = blockIdx.z;
   const int r0 = rt * kRows;
   const int plane = b * a.Hc + hc;
-  const int kvp = (hc * a.kv_mul) / a.kv_div;
-  const int kplane = b * a.kv_planes + kvp;
+  const int kplane = b * a.kv_planes + (hc * a.kv_mul) / a.kv_div;
 
-  // key-tile range
   const int r_last = min(r0 + kRows, a.Lq) - 1;
-  int nkeys;
-  if (PASS == 1) {
-    nkeys = live_keys(r_last, a.c_q, a.c_k, a.Lk, a.causal_mode);
-  } else {
-    const int i_max = r_last / a.rq;
-    nkeys = min(a.Lk, (i_max + 1) * a.rk);
-  }
+  const int nkeys = live_keys(r_last, a.c_q, a.c_k, a.Lk, a.causal_mode);
   const int n_tiles = (nkeys + kKeys - 1) / kKeys;
+  const int i_max = r_last / a.rq;
+  const int causal_keys = min(a.Lk, (i_max + 1) * a.rk);
+  const int n_part_tiles = min(n_tiles, (causal_keys + kKeys - 1) / kKeys);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar_q, 1);
-    for (int s = 0; s < kStages; ++s) {
+    mbar_init(&bar_q, 8);
+    for (int s = 0; s < kST; ++s) {
       mbar_init(&bar_kfull[s], 1);
       mbar_init(&bar_kempty[s], 1);
     }
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base_sh, 256);
+  if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -105,19 +109,13 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
-      tma_prefetch_desc(&tmQh);
       tma_prefetch_desc(&tmKh);
-      const int qrow = plane * a.Lq + r0;
-      mbar_arrive_expect_tx(&bar_q, 2 * L::kQBytes);
-      for (int kc = 0; kc < L::kChunks; ++kc) {
-        tma_load_2d(smem + L::kQOff + kc * kRows * 128, &tmQh, &bar_q, kc * 64, qrow);
-        tma_load_2d(smem + L::kQOff + L::kQBytes + kc * kRows * 128, &tmQl, &bar_q, kc * 64, qrow);
-      }
+      tma_prefetch_desc(&tmKl);
       const uint64_t pol = policy_evict_last();  // K tiles are re-read by every row tile
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % kStages;
-        if (t >= kStages) mbar_wait(&bar_kempty[s], ((t / kStages) + 1) & 1);
-        uint8_t* kh = smem + L::kKOff + s * 2 * L::kKBytes;
+        const int s = t % kST;
+        if (t >= kST) mbar_wait(&bar_kempty[s], ((t / kST) + 1) & 1);
+        uint8_t* kh = smem + s * 2 * L::kKBytes;
         uint8_t* kl = kh + L::kKBytes;
         mbar_arrive_expect_tx(&bar_kfull[s], 2 * L::kKBytes);
         const int krow = kplane * a.Lk + t * kKeys;
@@ -130,28 +128,27 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_f16(kRows, kKeys, /*f16*/ 0, false, false);
+    constexpr uint32_t idesc = idesc_f16(kRows, kKeys, /*f16*/ 0, false, false);
     mbar_wait(&bar_q, 0);
     tc_fence_after();
     for (int t = 0; t < n_tiles; ++t) {
-      const int s = t % kStages, buf = t & 1;
-      mbar_wait(&bar_kfull[s], (t / kStages) & 1);
-      if (t >= 2) mbar_wait(&bar_sempty[buf], ((t - 2) / 2) & 1);
+      const int s = t % kST, buf = t & 1;
+      mbar_wait(&bar_kfull[s], (t / kST) & 1);
+      if (t >= 2) mbar_wait(&bar_sempty[buf], ((t - 2) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t qh = smem_u32(smem + L::kQOff), ql = qh + L::kQBytes;
-        const uint32_t kh = smem_u32(smem + L::kKOff + s * 2 * L::kKBytes), kl = kh + L::kKBytes;
-        const uint32_t d_tmem = tmem + buf * kKeys;
+        const uint32_t kh = smem_u32(smem + s * 2 * L::kKBytes), kl = kh + L::kKBytes;
+        const uint32_t d_tmem = tmem + kTS0 + buf * kKeys;
 #pragma unroll
         for (int kc = 0; kc < L::kChunks; ++kc) {
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            const uint32_t qo = kc * kRows * 128 + ks * 32, ko = kc * kKeys * 128 + ks * 32;
-            const uint64_t aqh = sdesc_sw128(qh + qo, 16, 1024), aql = sdesc_sw128(ql + qo, 16, 1024);
+            const uint32_t ko = kc * kKeys * 128 + ks * 32;
+            const uint32_t qcol = (kc * 4 + ks) * 8;
             const uint64_t bkh = sdesc_sw128(kh + ko, 16, 1024), bkl = sdesc_sw128(kl + ko, 16, 1024);
-            umma_f16_ss(d_tmem, aqh, bkl, idesc, (kc | ks) != 0);
-            umma_f16_ss(d_tmem, aql, bkh, idesc, 1);
-            umma_f16_ss(d_tmem, aqh, bkh, idesc, 1);
+            umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkl, idesc, (kc | ks) != 0);
+            umma_f16_ts(d_tmem, tmem + kTQl + qcol, bkh, idesc, 1);
+            umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkh, idesc, 1);
           }
         }
         umma_commit(&bar_kempty[s]);
@@ -160,109 +157,155 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quarter
+    // ------------------------------------------------------------ epilogue groups
+    const int grp = (warp - 2) >> 2;  // 0: even tiles, 1: odd tiles
+    const int q = warp & 3;           // TMEM lane quarter
     const int row = q * 32 + lane;
     const int t_row = r0 + row;
     const bool row_ok = t_row < a.Lq;
+    const uint32_t lane_addr = tmem + (uint32_t(q * 32) << 16);
+    {
+      // Q hi (group 0) / Q lo (group 1) row -> TMEM, the A operand of every MMA
+      const __half* src = (grp == 0 ? a.qh : a.ql) + ((long long)plane * a.Lq + t_row) * D;
+      const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+      for (int c0 = 0; c0 < D / 2; c0 += 16) {
+        uint32_t w16[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint4 v = row_ok ? __ldg(s4 + c0 / 4 + u) : make_uint4(0, 0, 0, 0);
+          w16[4 * u] = v.x;
+          w16[4 * u + 1] = v.y;
+          w16[4 * u + 2] = v.z;
+          w16[4 * u + 3] = v.w;
+        }
+        tmem_st16(lane_addr + (grp == 0 ? kTQh : kTQl) + c0, w16);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_q);
+    }
     const int live = row_ok ? live_keys(t_row, a.c_q, a.c_k, a.Lk, a.causal_mode) : 0;
     const float k2 = ldexpf(a.scale_log2, -(a.exp_q[plane] + a.exp_k[kplane]));
-    const uint32_t lane_addr = tmem + (uint32_t(q * 32) << 16);
     float m = -INFINITY, l = 0.f;
-    const float lse2 = (PASS == 2 && row_ok) ? a.lse2[(long long)plane * a.Lq + t_row] : 0.f;
-    for (int t = 0; t < n_tiles; ++t) {
-      const int buf = t & 1;
-      mbar_wait(&bar_sfull[buf], (t / 2) & 1);
+    for (int t = grp; t < n_tiles; t += 2) {
+      mbar_wait(&bar_sfull[grp], (t >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int ch = 0; ch < kKeys / 32; ++ch) {
-        uint32_t v[32];
-        tmem_ld32(lane_addr + buf * kKeys + ch * 32, v);
-        tmem_ld_wait();
-        if (ch == kKeys / 32 - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_sempty[buf]);
+      uint32_t v[kKeys];
+      {
+        uint32_t* v0 = v;
+        tmem_ld32(lane_addr + kTS0 + grp * kKeys + 0, *reinterpret_cast<uint32_t(*)[32]>(v0));
+        tmem_ld32(lane_addr + kTS0 + grp * kKeys + 32, *reinterpret_cast<uint32_t(*)[32]>(v0 + 32));
+        tmem_ld32(lane_addr + kTS0 + grp * kKeys + 64, *reinterpret_cast<uint32_t(*)[32]>(v0 + 64));
+        tmem_ld32(lane_addr + kTS0 + grp * kKeys + 96, *reinterpret_cast<uint32_t(*)[32]>(v0 + 96));
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_sempty[grp]);
+
+      const int nvalid = min(max(live - t * kKeys, 0), kKeys);
+      float x[kKeys];
+      float m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kKeys; ++c) {
+        x[c] = c < nvalid ? __uint_as_float(v[c]) * k2 : -INFINITY;
+        m8[c & 7] = fmaxf(m8[c & 7], x[c]);
+      }
+      const float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      // slot sums (fixed pairwise order inside each slot of SW keys)
+      float slot[NS];
+      if (mt == -INFINITY) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) slot[s] = 0.f;
+      } else {
+        const float2 nm = make_float2(-mt, -mt);
+#pragma unroll
+        for (int c = 0; c < kKeys; c += 2) {
+          const float2 d2 = __fadd2_rn(make_float2(x[c], x[c + 1]), nm);
+          x[c] = ex2_approx(d2.x);
+          x[c + 1] = ex2_approx(d2.y);
         }
-        const int key0 = t * kKeys + ch * 32;
-        if (PASS == 1) {
-          float x[32];
-          float cm = -INFINITY;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            x[c] = (key0 + c < live) ? __uint_as_float(v[c]) * k2 : -INFINITY;
-            cm = fmaxf(cm, x[c]);
-          }
-          const float m_new = fmaxf(m, cm);
-          if (m_new != -INFINITY) {
-            float sum = 0.f;
+        for (int w = 1; w < SW; w <<= 1)
 #pragma unroll
-            for (int c = 0; c < 32; ++c) sum += ex2_approx(x[c] - m_new);
-            l = l * ex2_approx(m - m_new) + sum;
-            m = m_new;
-          }
-        } else {
-          float v32[32];
+          for (int c = 0; c < kKeys; c += 2 * w) x[c] += x[c + w];
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            v32[c] = (key0 + c < live) ? ex2_approx(fmaf(__uint_as_float(v[c]), k2, -lse2)) : 0.f;
-          // pairwise tree inside groups of min(rk, 32) keys (register indices are
-          // compile-time; the runtime rk only predicates whole levels)
+        for (int s = 0; s < NS; ++s) slot[s] = x[s * SW];
+      }
+      float tot = 0.f;
+      {
+        float acc4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int w = 1; w < 32; w <<= 1) {
-            if (w < a.rk) {
+        for (int s = 0; s < NS; ++s) acc4[s & 3] += slot[s];
+        tot = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+      }
+      if (mt > m) {
+        l = l * ex2_approx(m - mt) + tot;
+        m = mt;
+      } else if (mt != -INFINITY) {
+        l += tot * ex2_approx(mt - m);
+      }
+      if (t < n_part_tiles && row_ok) {
+        const long long prow = ((long long)plane * a.T + t) * a.Lq + t_row;
+        float4* dst = reinterpret_cast<float4*>(a.part + prow * NS);
 #pragma unroll
-              for (int c = 0; c < 32; c += 2 * w) v32[c] += v32[c + w];
-            }
-          }
-          // stage this row's key-group partials of the current segment in smem
-          const int cps = min(4, a.rk);            // chunks per segment
-          const int gseg = (32 * cps) / a.rk;      // key groups per segment (<= 32)
-          const int cseg = ch % cps;               // chunk index inside the segment
-          if (a.rk <= 32) {
-            const int ng = 32 / a.rk;
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if ((c & (a.rk - 1)) == 0) red[row][cseg * ng + c / a.rk] = v32[c];
-          } else {
-            const int gi = (cseg * 32) / a.rk;     // group inside the segment
-            if ((cseg * 32) % a.rk == 0) red[row][gi] = v32[0];
-            else red[row][gi] += v32[0];
-          }
-          if (cseg == cps - 1) {
-            // cross-row sums over the rq rows of each query block, fixed order,
-            // consecutive threads -> consecutive key blocks (coalesced stores)
-            named_bar_sync(1, 128);
-            const int qb_tile = kRows / a.rq;
-            const int nout = qb_tile * gseg;
-            const int j0 = (t * kKeys + (ch - cseg) * 32) / a.rk;
-            for (int o = row; o < nout; o += 128) {
-              const int qb = o / gseg, gg = o % gseg;
-              float sum = 0.f;
-              for (int r = 0; r < a.rq; ++r) sum += red[qb * a.rq + r][gg];
-              const int i = (r0 / a.rq) + qb;
-              const int j = j0 + gg;
-              if (qb * a.rq + r0 < a.Lq && j <= i)
-                a.scores[((long long)plane * a.N + i) * a.N + j] = sum;
-            }
-            named_bar_sync(1, 128);
-          }
-        }
+        for (int s = 0; s < NS; s += 4) dst[s / 4] = make_float4(slot[s], slot[s + 1], slot[s + 2], slot[s + 3]);
+        a.tmax[prow] = mt;
       }
     }
-    if (PASS == 1 && row_ok) a.lse2[(long long)plane * a.Lq + t_row] = m + __log2f(l);
+    // merge the two groups' online (max, sum) per row -> row LSE in log2 units
+    if (grp == 1) ml_sh[row] = make_float2(m, l);
+    named_bar_sync(1, 256);
+    if (grp == 0 && row_ok) {
+      const float2 o = ml_sh[row];
+      const float M = fmaxf(m, o.x);
+      const float lt = (m == -INFINITY ? 0.f : l * ex2_approx(m - M)) + (o.x == -INFINITY ? 0.f : o.y * ex2_approx(o.x - M));
+      a.lse2[(long long)plane * a.Lq + t_row] = M + __log2f(lt);
+    }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-template <int D, int PASS>
-us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmQh, const CUtensorMap& tmQl,
-                         const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
+// score(i, j) for j <= i from the slot partials (fixed row order r = 0..rq-1,
+// slots of a key block in ascending order). CTA = (query block i, plane).
+template <int SW>
+__global__ void __launch_bounds__(256) proxy_finalize_kernel(const ProxyArgs a) {
+  constexpr int NS = kKeys / SW;
+  __shared__ float lse_sh[64];
+  const int i = gridDim.x - 1 - blockIdx.x;
+  const int plane = blockIdx.y;
+  const int row0 = i * a.rq;
+  if (threadIdx.x < a.rq) lse_sh[threadIdx.x] = a.lse2[(long long)plane * a.Lq + row0 + threadIdx.x];
+  __syncthreads();
+  const int spb = a.rk / SW;  // slots per key block
+  float* out = a.scores + ((long long)plane * a.N + i) * a.N;
+  for (int j = threadIdx.x; j <= i; j += blockDim.x) {
+    const int key0 = j * a.rk;
+    const int t = key0 / kKeys, s0 = (key0 % kKeys) / SW;
+    const long long base = ((long long)plane * a.T + t) * a.Lq + row0;
+    float acc = 0.f;
+    for (int r = 0; r < a.rq; ++r) {
+      const float* pr = a.part + (base + r) * NS + s0;
+      float ps = 0.f;
+      for (int u = 0; u < spb; ++u) ps += pr[u];
+      acc += ps * ex2_approx(a.tmax[base + r] - lse_sh[r]);
+    }
+    out[j] = acc;
+  }
+}
+
+template <int D, int SW>
+us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
   const int smem = ProxySmem<D>::kBytes + 1024;
-  auto kern = proxy_kernel<D, PASS>;
+  auto kern = proxy_kernel<D, SW>;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     US_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -270,22 +313,37 @@ us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmQh, const CUte
     attr_set = true;
   }
   dim3 grid((a.Lq + kRows - 1) / kRows, a.Hc, a.B);
-  kern<<<grid, 192, smem, st>>>(tmQh, tmQl, tmKh, tmKl, a);
+  kern<<<grid, 320, smem, st>>>(tmKh, tmKl, a);
   US_LAUNCH_CHECK("proxy_kernel");
+  proxy_finalize_kernel<SW><<<dim3(a.N, a.B * a.Hc), 256, 0, st>>>(a);
+  US_LAUNCH_CHECK("proxy_finalize_kernel");
   return US_OK;
+}
+
+template <int D>
+us_status launch_proxy_d(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
+  switch (a.sw) {
+    case 8: return launch_proxy_t<D, 8>(a, tmKh, tmKl, st);
+    case 4: return launch_proxy_t<D, 4>(a, tmKh, tmKl, st);
+    case 2: return launch_proxy_t<D, 2>(a, tmKh, tmKl, st);
+    case 1: return launch_proxy_t<D, 1>(a, tmKh, tmKl, st);
+    default:
+      set_error("proxy: unsupported slot width");
+      return US_ERR_UNSUPPORTED;
+  }
 }
 
 }  // namespace
 
-us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmQh, const CUtensorMap& tmQl,
-                       const CUtensorMap& tmKh, const CUtensorMap& tmKl, int pass,
-                       cudaStream_t st) {
-  if (a.D == 128)
-    return pass == 1 ? launch_proxy_t<128, 1>(a, tmQh, tmQl, tmKh, tmKl, st)
-                     : launch_proxy_t<128, 2>(a, tmQh, tmQl, tmKh, tmKl, st);
-  if (a.D == 64)
-    return pass == 1 ? launch_proxy_t<64, 1>(a, tmQh, tmQl, tmKh, tmKl, st)
-                     : launch_proxy_t<64, 2>(a, tmQh, tmQl, tmKh, tmKl, st);
+int proxy_slot_width(int rk) { return rk >= 8 ? 8 : rk; }
+
+us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
+  if (a.rq > 64) {
+    set_error("proxy: S/c_q above 64 unsupported");
+    return US_ERR_UNSUPPORTED;
+  }
+  if (a.D == 128) return launch_proxy_d<128>(a, tmKh, tmKl, st);
+  if (a.D == 64) return launch_proxy_d<64>(a, tmKh, tmKl, st);
   set_error("proxy: d_k must be 64 or 128 on the GPU path");
   return US_ERR_UNSUPPORTED;
 }
