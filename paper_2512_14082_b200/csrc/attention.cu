@@ -44,11 +44,11 @@
 #define US_ATTN_TRACE 0
 #endif
 #if US_ATTN_TRACE
-__device__ long long g_attn_trace[2 * 4096 * 8];
+__device__ long long g_attn_trace[2 * 4096 * 16];
 __device__ int g_attn_trace_cta;
 #define TRACE(x, k, e)                                                                  \
   do {                                                                                  \
-    if (blockIdx.x == g_attn_trace_cta && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 8 + (e)] = clock64(); \
+    if (blockIdx.x == g_attn_trace_cta && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 16 + (e)] = clock64(); \
   } while (0)
 #else
 #define TRACE(x, k, e) \
@@ -97,7 +97,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-constexpr int kPolyFrom = 48;  // columns [48, 64) of an off-diagonal tile use ex2_poly2 (25%)
+#ifndef US_ATTN_POLY_FROM
+#define US_ATTN_POLY_FROM 48
+#endif
+// columns [kPolyFrom, 64) of an off-diagonal tile use ex2_poly2 (FMA pipe)
+constexpr int kPolyFrom = US_ATTN_POLY_FROM;
 
 // Work order: KV head outermost, query blocks heaviest-first inside it, so the
 // ~148 resident CTAs all stream K/V of ONE KV head (L * d * 4 bytes = 64 MB at
@@ -538,7 +542,7 @@ us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUte
 
 #if US_ATTN_TRACE
 extern "C" int us_debug_attn_trace(int cta, long long* host_out) {
-  if (host_out) return int(cudaMemcpyFromSymbol(host_out, ::g_attn_trace, sizeof(long long) * 2 * 4096 * 8));
+  if (host_out) return int(cudaMemcpyFromSymbol(host_out, ::g_attn_trace, sizeof(long long) * 2 * 4096 * 16));
   return int(cudaMemcpyToSymbol(::g_attn_trace_cta, &cta, sizeof(int)));
 }
 #endif

@@ -13,9 +13,9 @@ eng.run(dense=True); torch.cuda.synchronize()
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 L.us_debug_attn_trace(cta, None)
 eng.run(dense=True); torch.cuda.synchronize()
-buf = np.zeros(2 * 4096 * 8, np.int64)
+buf = np.zeros(2 * 4096 * 16, np.int64)
 L.us_debug_attn_trace(cta, buf.ctypes.data)
-tr = buf.reshape(2, 4096, 8)
+tr = buf.reshape(2, 4096, 16)
 n = int((tr[0, :, 0] > 0).sum())
 t0 = tr[:, :n, :4][tr[:, :n, :4] > 0].min()
 print(f"cta {cta}: {n} steps per tile")
