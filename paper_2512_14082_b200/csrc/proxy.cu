@@ -276,27 +276,45 @@ __global__ void __launch_bounds__(320, 1)
 
 // score(i, j) for j <= i from the slot partials (fixed row order r = 0..rq-1,
 // slots of a key block in ascending order). CTA = (query block i, plane).
-template <int SW>
+// RQ / SPB > 0: compile-time rows per query block / slots per key block (the
+// c = 8 fast path: every load of a score issued before its first use).
+template <int SW, int RQ, int SPB>
 __global__ void __launch_bounds__(256) proxy_finalize_kernel(const ProxyArgs a) {
   constexpr int NS = kKeys / SW;
   __shared__ float lse_sh[64];
   const int i = gridDim.x - 1 - blockIdx.x;
   const int plane = blockIdx.y;
-  const int row0 = i * a.rq;
-  if (threadIdx.x < a.rq) lse_sh[threadIdx.x] = a.lse2[(long long)plane * a.Lq + row0 + threadIdx.x];
+  const int rq = RQ > 0 ? RQ : a.rq;
+  const int spb = SPB > 0 ? SPB : a.rk / SW;  // slots per key block
+  const int row0 = i * rq;
+  if (threadIdx.x < rq) lse_sh[threadIdx.x] = a.lse2[(long long)plane * a.Lq + row0 + threadIdx.x];
   __syncthreads();
-  const int spb = a.rk / SW;  // slots per key block
   float* out = a.scores + ((long long)plane * a.N + i) * a.N;
   for (int j = threadIdx.x; j <= i; j += blockDim.x) {
     const int key0 = j * a.rk;
     const int t = key0 / kKeys, s0 = (key0 % kKeys) / SW;
     const long long base = ((long long)plane * a.T + t) * a.Lq + row0;
     float acc = 0.f;
-    for (int r = 0; r < a.rq; ++r) {
-      const float* pr = a.part + (base + r) * NS + s0;
-      float ps = 0.f;
-      for (int u = 0; u < spb; ++u) ps += pr[u];
-      acc += ps * ex2_approx(a.tmax[base + r] - lse_sh[r]);
+    if (RQ > 0 && SPB > 0) {
+      constexpr int R = RQ > 0 ? RQ : 1;
+      float pm[R], ps[R];
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        pm[r] = __ldg(a.tmax + base + r);
+        float v = 0.f;
+#pragma unroll
+        for (int u = 0; u < SPB; ++u) v += __ldg(a.part + (base + r) * NS + s0 + u);
+        ps[r] = v;
+      }
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) acc += ps[r] * ex2_approx(pm[r] - lse_sh[r]);
+    } else {
+      for (int r = 0; r < rq; ++r) {
+        const float* pr = a.part + (base + r) * NS + s0;
+        float v = 0.f;
+        for (int u = 0; u < spb; ++u) v += pr[u];
+        acc += v * ex2_approx(a.tmax[base + r] - lse_sh[r]);
+      }
     }
     out[j] = acc;
   }
@@ -315,7 +333,9 @@ us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmKh, const CUte
   dim3 grid((a.Lq + kRows - 1) / kRows, a.Hc, a.B);
   kern<<<grid, 320, smem, st>>>(tmKh, tmKl, a);
   US_LAUNCH_CHECK("proxy_kernel");
-  proxy_finalize_kernel<SW><<<dim3(a.N, a.B * a.Hc), 256, 0, st>>>(a);
+  const dim3 fgrid(a.N, a.B * a.Hc);
+  if (SW == 8 && a.rq == 8 && a.rk == 8) proxy_finalize_kernel<SW, 8, 1><<<fgrid, 256, 0, st>>>(a);
+  else proxy_finalize_kernel<SW, 0, 0><<<fgrid, 256, 0, st>>>(a);
   US_LAUNCH_CHECK("proxy_finalize_kernel");
   return US_OK;
 }

@@ -9,8 +9,10 @@
 // GPU algorithm (one warp per row, scores as f32 bit patterns in registers —
 // non-negative floats order like their unsigned bits):
 //   1. total = fp64 warp sum (fixed tree).
-//   2. binary search over the 31 value bits for v* = the largest value whose
-//      tail mass G(v*) = sum_{x >= v*} x reaches T = P * total (top-k: tail count).
+//   2. bisection over the value bits for v* = the largest value whose tail mass
+//      G(v*) = sum_{x >= v*} x reaches T = P * total, with fp32 tail sums (cheap;
+//      a candidate that fp32 rounding put on the wrong side of T is caught by the
+//      certification below); top-k: bisection on the tail count.
 //   3. A = sum_{x > v*} x; walk the ties of v* in index order: cum = A + v*,
 //      A + 2v*, ... until cum >= T — exactly the reference walk across the
 //      boundary group.
@@ -34,6 +36,11 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+__device__ __forceinline__ float warp_sum_f32(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 __device__ __forceinline__ int warp_sum_i32(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -41,7 +48,7 @@ __device__ __forceinline__ int warp_sum_i32(int v) {
 }
 
 template <int NPL>
-__global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
+__global__ void __launch_bounds__(256, 2) select_kernel(SelectArgs a) {
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -86,7 +93,7 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
 #pragma unroll
         for (int k = 0; k < NPL; ++k)
           if (k * 32 < n) cnt += (k * 32 + lane < n && bits[k] >= cand) ? 1 : 0;
-        if (warp_sum_i32(cnt) >= kk) bstar = cand;
+        if (int(__reduce_add_sync(0xffffffffu, unsigned(cnt))) >= kk) bstar = cand;
       }
       int gt = 0;
 #pragma unroll
@@ -102,14 +109,26 @@ __global__ void __launch_bounds__(256) select_kernel(SelectArgs a) {
       mode = 1;
     } else {
       const double T = a.P * total;
-      for (int bit = 30; bit >= 0; --bit) {
+      // (a) candidate v* by bisection over the value bits with fp32 tail sums
+      //     (4 independent accumulators per lane, fixed shuffle tree) — cheap, but
+      //     only approximately ordered against T;
+      const float Tf = float(T);
+      uint32_t mx = 0;
+#pragma unroll
+      for (int k = 0; k < NPL; ++k) mx = max(mx, bits[k]);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      const int top = 31 - __clz(mx | 1u);
+      for (int bit = top; bit >= 0; --bit) {
         const uint32_t cand = bstar | (1u << bit);
-        double g = 0.0;
+        float g8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < NPL; ++k)
-          if (k * 32 < n && k * 32 + lane < n && bits[k] >= cand) g += double(__uint_as_float(bits[k]));
-        if (warp_sum_f64(g) >= T) bstar = cand;
+          if (k * 32 < n) g8[k & 7] += bits[k] >= cand ? __uint_as_float(bits[k]) : 0.f;
+        const float g = ((g8[0] + g8[1]) + (g8[2] + g8[3])) + ((g8[4] + g8[5]) + (g8[6] + g8[7]));
+        if (warp_sum_f32(g) >= Tf) bstar = cand;
       }
+      // (b) exact fp64 boundary walk + certification (a wrong candidate from (a)
+      //     fails certification and goes to the verbatim reference walk).
       double A = 0.0;
       int E = 0;
 #pragma unroll
