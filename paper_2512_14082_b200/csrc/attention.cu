@@ -19,16 +19,24 @@
 // not select a block visited by its tile contributes P = 0 rows, so each
 // group's output equals sparse attention over exactly its own selection.
 //
-// Roles (384 threads): warp 0 TMA producer (6-stage K/V ring), warps 1 / 3
+// Roles (384 threads): warp 0 TMA producer (5-stage K/V ring), warps 1 / 3
 // MMA issuers of tile A / B (warp 1 owns TMEM), warp 2 builds the union list,
 // warps 4-7 softmax of tile A, warps 8-11 softmax of tile B (thread = row).
-// TMEM per tile X (256 cols at X*256): S [0,64) fp32 with P (bf16x2) aliased
-// into [0,32) after the row is read, O [64,192), Q [192,256) (bf16x2, A operand
-// of S = Q K^T). Both MMAs are TS-mode (A from TMEM); only K/V come from smem.
-// Per tile the tensor pipe runs ... S(k) | P.V(k) S(k+1) | P.V(k+1) ... in
-// issue order; the two tiles ping-pong so one softmax overlaps the other
-// tile's MMAs (the tile issuers are independent warps). The S(k+1) commit retires P.V(k) too (commit covers all prior
-// MMAs), so O rescales and P/S aliasing need no extra barriers.
+// TMEM per tile X (256 cols at X*256): S [0,64) fp32, O [64,192), Q [192,256)
+// (bf16x2, A operand of S = Q K^T, TS-mode MMA). P (bf16) goes to a
+// 128 x 64 SWIZZLE_128B tile in SMEM and P.V is an SS-mode MMA, so the S
+// columns are free as soon as the softmax has LOADED S(k): the issuer starts
+// S(k+1) right then, and the tensor pipe computes the next logits while the
+// softmax is still exponentiating — the S -> softmax -> P.V round trip no
+// longer serialises each tile (r01d: the v6 step was ~3000 cycles for 622
+// cycles of MMA). The issuer releases every union position in order (used ones
+// by the P.V commit, skipped ones by a plain arrive); S(k+1) is issued early
+// only when the next own position is < kST positions ahead, otherwise after
+// P.V(k) (its ring stage may be the one P.V(k) frees).
+// P.V(k) commits bar_pvdone: the softmax waits for P.V(k-1) before it
+// overwrites the single P buffer or rescales O (both only touch state P.V(k-1)
+// reads / writes; P.V(k-2) is always complete by then — it was issued before
+// S(k) — so the parity wait is never more than one phase behind).
 // Online softmax in log2 units with lazy rescaling: the running max used for
 // exponentiation only moves when a row max exceeds it by > 8 (p <= 2^8).
 #include "host_util.hpp"
@@ -66,18 +74,19 @@ constexpr int kMaxW = kMaxN / 32;
 // K/V ring depth: a 64-key K+V tile takes ~1-2 us to land from L2, so the ring
 // must cover several steps of prefetch.
 template <int D>
-constexpr int stages_for() { return D == 128 ? 6 : 10; }
+constexpr int stages_for() { return D == 128 ? 5 : 10; }
 
 template <int D>
 struct AttnSmem {
   static constexpr int kST = stages_for<D>();
   static constexpr int kChunks = D / 64;
-  static constexpr int kKVBytes = kBS * D * 2;  // one of K / V per stage
-  static constexpr int kBytes = kST * 2 * kKVBytes;
+  static constexpr int kKVBytes = kBS * D * 2;       // one of K / V per stage
+  static constexpr int kRingBytes = kST * 2 * kKVBytes;
+  static constexpr int kPBytes = 128 * kBS * 2;      // per tile: 128 rows x 64 keys bf16
+  static constexpr int kBytes = kRingBytes + 2 * kPBytes;
 };
 
-// TMEM columns of tile X start at X * 256: S [0,64) (P aliased into [0,32)),
-// O [64, 64+D), Q [192, 192+D/2).
+// TMEM columns of tile X start at X * 256: S [0,64), O [64, 64+D), Q [192, 192+D/2).
 constexpr uint32_t kTS = 0, kTO = 64, kTQ = 192;
 
 // exp2 on the FMA/ALU pipes for a pair of values (offloads MUFU): round-to-nearest
@@ -161,7 +170,8 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int kST = SL::kST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q[2], bar_kvfull[kST], bar_kvempty[kST], bar_sfull[2], bar_pfull[2], bar_ofull[2];
+  __shared__ uint64_t bar_q[2], bar_kvfull[kST], bar_kvempty[kST], bar_sfull[2], bar_sfree[2], bar_pfull[2],
+      bar_pvdone[2], bar_ofull[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int n_steps_sh;
   __shared__ uint32_t mrow[4][kMaxW];
@@ -180,7 +190,9 @@ __global__ void __launch_bounds__(384, 1)
     for (int x = 0; x < 2; ++x) {
       mbar_init(&bar_q[x], 4);
       mbar_init(&bar_sfull[x], 1);
+      mbar_init(&bar_sfree[x], 4);
       mbar_init(&bar_pfull[x], 4);
+      mbar_init(&bar_pvdone[x], 1);
     }
     for (int s = 0; s < kST; ++s) {
       mbar_init(&bar_kvfull[s], 1);
@@ -266,29 +278,30 @@ __global__ void __launch_bounds__(384, 1)
     __syncwarp();
   } else if (warp == 1 || warp == 3) {
     // ------------------------------------------------------------ MMA issuers
-    // One issuer warp per tile (warp 1 -> A, warp 3 -> B): S(k), P.V(k), S(k+1), ...
-    // strictly alternating (P(k) aliases S(k)), releasing every union position in
-    // order — used ones by the P.V commit, skipped ones by a plain arrive — so the
-    // two tiles never wait on each other and the producer always makes progress.
     const int x = warp == 1 ? 0 : 1;
     constexpr uint32_t idesc_s = idesc_f16(128, kBS, /*bf16*/ 1, false, false);
     constexpr uint32_t idesc_o = idesc_f16(128, D, /*bf16*/ 1, false, /*V MN-major*/ true);
     const uint32_t tb = tmem + x * 256;
-    mbar_wait(&bar_q[x], 0);  // Q rows of tile x are in TMEM
-    tc_fence_after();
-    int k = 0;
-    for (int t = 0; t < T; ++t) {
-      const int st = t % kST;
-      // Waiting for the tile to land even when skipping keeps this warp's
-      // kv_empty arrivals in phase order (one per stage phase).
-      mbar_wait(&bar_kvfull[st], (t / kST) & 1);
-      if (((steps[t] >> (16 + 2 * x)) & 3u) == 0u) {
-        if (lane == 0) mbar_arrive(&bar_kvempty[st]);  // not needed by this tile
-        continue;
+    const uint32_t sP = smem_u32(smem + SL::kRingBytes + x * SL::kPBytes);
+    auto own = [&](int tt) { return ((steps[tt] >> (16 + 2 * x)) & 3u) != 0u; };
+    auto next_own = [&](int from) {
+      int tt = from;
+      while (tt < T && !own(tt)) ++tt;
+      return tt;
+    };
+    // Release union positions [from, to) this tile skips. Waiting for each tile to
+    // land keeps this warp's kv_empty arrivals in phase order (one per stage phase).
+    auto release = [&](int from, int to) {
+      for (int tt = from; tt < to; ++tt) {
+        mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
+        if (lane == 0) mbar_arrive(&bar_kvempty[tt % kST]);
       }
+    };
+    auto issue_s = [&](int tt, int kk) {
+      mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sK = smem_u32(smem + st * 2 * SL::kKVBytes);
+        const uint32_t sK = smem_u32(smem + (tt % kST) * 2 * SL::kKVBytes);
 #pragma unroll
         for (int kc = 0; kc < SL::kChunks; ++kc)
 #pragma unroll
@@ -297,22 +310,44 @@ __global__ void __launch_bounds__(384, 1)
             umma_f16_ts(tb + kTS, tb + kTQ + (kc * 4 + ks) * 8, bd, idesc_s, (kc | ks) != 0);
           }
         umma_commit(&bar_sfull[x]);
-        TRACE(x, k, 0);
+        TRACE(x, kk, 0);
       }
       __syncwarp();
-      mbar_wait(&bar_pfull[x], k & 1);
+    };
+    mbar_wait(&bar_q[x], 0);  // Q rows of tile x are in TMEM
+    tc_fence_after();
+    int t = next_own(0);
+    release(0, t);
+    if (t < T) issue_s(t, 0);
+    int k = 0;
+    while (t < T) {
+      const int tn = next_own(t + 1);
+      const bool early = tn < T && tn - t < kST;
+      mbar_wait(&bar_sfree[x], k & 1);  // the softmax has loaded S(k): S columns are free
+      if (early) {
+        release(t + 1, tn);
+        issue_s(tn, k + 1);
+      }
+      mbar_wait(&bar_pfull[x], k & 1);  // P(k) is in SMEM
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sV = smem_u32(smem + st * 2 * SL::kKVBytes + SL::kKVBytes);
+        const uint32_t sV = smem_u32(smem + (t % kST) * 2 * SL::kKVBytes + SL::kKVBytes);
 #pragma unroll
         for (int ks = 0; ks < kBS / 16; ++ks) {
+          const uint64_t ad = sdesc_sw128(sP + ks * 32, 16, 1024);
           const uint64_t bd = sdesc_sw128(sV + ks * 16 * 128, kBS * 128, 1024);
-          umma_f16_ts(tb + kTO, tb + kTS + ks * 8, bd, idesc_o, (k > 0 || ks > 0) ? 1u : 0u);
+          umma_f16_ss(tb + kTO, ad, bd, idesc_o, (k > 0 || ks > 0) ? 1u : 0u);
         }
-        umma_commit(&bar_kvempty[st]);
+        umma_commit(&bar_kvempty[t % kST]);
+        umma_commit(&bar_pvdone[x]);
         TRACE(x, k, 3);
       }
       __syncwarp();
+      if (!early) {
+        release(t + 1, tn);
+        if (tn < T) issue_s(tn, k + 1);
+      }
+      t = tn;
       ++k;
     }
     if (elect_one()) umma_commit(&bar_ofull[x]);
@@ -327,6 +362,7 @@ __global__ void __launch_bounds__(384, 1)
     const bool en = gr.en[g];
     const uint32_t lane_addr = uint32_t(q * 32) << 16;
     const uint32_t tb = tmem + lane_addr + x * 256;
+    const uint32_t prow = smem_u32(smem + SL::kRingBytes + x * SL::kPBytes + row * 128);  // this row of the P tile
     const float sl2 = a.scale_log2;
     float m_used = -INFINITY, l = 0.f;
     {
@@ -372,23 +408,13 @@ __global__ void __launch_bounds__(384, 1)
           sv[32 + c] = __uint_as_float(v2[c]);
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_sfree[x]);  // S(k+1) may now overwrite the S columns
       if (row == 0) TRACE(x, k, 4);
+      bool pv_prev_done = (k == 0);
       uint32_t packed[kBS / 2];
-#if US_ATTN_SKELETON
-      // calibration build only: keep the data movement and synchronisation, drop the math
       if (sel) {
-        l += sv[0] + sv[63];
-#pragma unroll
-        for (int c = 0; c < kBS / 2; ++c) packed[c] = 0x3f803f80u;
-        m_used = 0.f;
-      } else {
-#pragma unroll
-        for (int c = 0; c < kBS / 2; ++c) packed[c] = 0u;
-      }
-      if (false) {
-#else
-      if (sel) {
-#endif
         const bool diag = (j == ig);
         if (diag) {
 #pragma unroll
@@ -408,10 +434,14 @@ __global__ void __launch_bounds__(384, 1)
         mx *= sl2;
         const bool need = mx > m_used + 8.f;
         const bool need_o = need && l > 0.f;
-        // tcgen05.ld/st are warp-collective: the O pass runs for the whole warp
-        // whenever any of its rows moves its max; other rows use f = 1. P.V(k-1)
-        // has retired: the S(k) commit covers it.
+        // O rescale (warp-collective TMEM ld/st) once P.V(k-1) has retired; rows
+        // that did not move use f = 1.
         if (__any_sync(0xffffffffu, need_o)) {
+          if (!pv_prev_done) {
+            mbar_wait(&bar_pvdone[x], (k - 1) & 1);
+            tc_fence_after();
+            pv_prev_done = true;
+          }
           const float f = need_o ? ex2_approx(m_used - mx) : 1.f;
 #pragma unroll 1
           for (int c0 = 0; c0 < D; c0 += 32) {
@@ -462,10 +492,14 @@ __global__ void __launch_bounds__(384, 1)
         for (int c = 0; c < kBS / 2; ++c) packed[c] = 0u;
       }
       if (row == 0) TRACE(x, k, 5);
-      US_TMEM_ST_X32(tb + kTS, packed);  // P aliases the S columns just read
-      tmem_st_wait();
-      if (row == 0) TRACE(x, k, 6);
-      tc_fence_before();
+      // P(k) -> the SWIZZLE_128B P tile (row = 128 B = 8 chunks of 16 B); P.V(k-1)
+      // must have consumed P(k-1) first
+      if (!pv_prev_done) mbar_wait(&bar_pvdone[x], (k - 1) & 1);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        st_shared_v4(prow + ((c ^ (row & 7)) << 4), packed[4 * c], packed[4 * c + 1], packed[4 * c + 2],
+                     packed[4 * c + 3]);
+      fence_proxy_async_smem();
       __syncwarp();
       if (row == 0) TRACE(x, k, 2);
       if (lane == 0) mbar_arrive(&bar_pfull[x]);
@@ -508,7 +542,7 @@ __global__ void __launch_bounds__(384, 1)
 template <int D>
 us_status launch_attn_t(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                         const CUtensorMap& tmV, cudaStream_t st) {
-  const int smem = AttnSmem<D>::kBytes + 1024;
+  const int smem = AttnSmem<D>::kBytes + 1024;  // + alignment slack
   static bool attr_set = false;
   if (!attr_set) {
     US_CUDA_TRY(cudaFuncSetAttribute(attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),

@@ -283,3 +283,65 @@ extern "C" us_status us_selftest_tmem_ld(int iters, int mma_n, int ctas, float* 
   US_LAUNCH_CHECK("us_selftest_tmem_ld");
   return US_OK;
 }
+
+// ---------------------------------------------------------------- exp2 throughput probe
+// Each thread runs `iters` rounds of 32 independent exp2 evaluations
+// (mode 0: MUFU ex2.approx; mode 1: the FMA-pipe cubic of attention.cu;
+// mode 2: FFMA2 only, as a pipe-rate reference). Output: cycles per CTA.
+namespace us {
+namespace {
+__device__ __forceinline__ float2 probe_poly2(float2 x) {
+  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
+  float2 p = __ffma2_rn(make_float2(0.0551f, 0.0551f), f, make_float2(0.2426f, 0.2426f));
+  p = __ffma2_rn(p, f, make_float2(0.6933f, 0.6933f));
+  p = __ffma2_rn(p, f, make_float2(0.9999f, 0.9999f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+__global__ void ex2_rate_kernel(int iters, int mode, float* sink, long long* cycles_out) {
+  float v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = -0.001f * float(threadIdx.x + c);
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    if (mode == 0) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = ex2_approx(v[c]) - 1.0f;
+    } else if (mode == 1) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const float2 p = probe_poly2(make_float2(v[c], v[c + 1]));
+        v[c] = p.x - 1.0f;
+        v[c + 1] = p.y - 1.0f;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        const float2 p = __ffma2_rn(make_float2(v[c], v[c + 1]), make_float2(0.999f, 0.999f),
+                                    make_float2(0.001f, 0.001f));
+        v[c] = p.x;
+        v[c + 1] = p.y;
+      }
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) s += v[c];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cycles_out[blockIdx.x] = t1 - t0;
+}
+}  // namespace
+}  // namespace us
+
+extern "C" us_status us_selftest_ex2_rate(int iters, int mode, int ctas, int threads, float* sink,
+                                          long long* cycles_out, void* stream) {
+  using namespace us;
+  ex2_rate_kernel<<<ctas, threads, 0, static_cast<cudaStream_t>(stream)>>>(iters, mode, sink, cycles_out);
+  US_LAUNCH_CHECK("us_selftest_ex2_rate");
+  return US_OK;
+}

@@ -23,7 +23,7 @@ for k in list(range(0, 6)) + list(range(n // 2, n // 2 + 6)):
     a, b = tr[0, k, :4] - t0, tr[1, k, :4] - t0
     print(f"k={k:4d}  A: S@{a[0]:8d} seen@{a[1]:8d} P@{a[2]:8d} PV@{a[3]:8d} |  B: S@{b[0]:8d} seen@{b[1]:8d} P@{b[2]:8d} PV@{b[3]:8d}")
 d = np.diff(tr[0, :n, 0]); print("tile A cycles/step (median):", np.median(d))
-for name, (e0, e1) in {"S issue -> seen": (0, 1), "seen -> S loaded (LDTM)": (1, 4), "loaded -> math done": (4, 5), "STTM P + wait": (5, 6), "st done -> P ready": (6, 2), "P ready -> PV issued": (2, 3), "PV issued -> next S issue": (3, 0)}.items():
+for name, (e0, e1) in {"S issue -> seen": (0, 1), "seen -> S loaded (LDTM)": (1, 4), "loaded -> math done": (4, 5), "P to smem + fence": (5, 2), "P ready -> PV issued": (2, 3), "PV issued -> next S issue": (3, 0)}.items():
     if e1 == 0:
         v = tr[0, 1:n, 0] - tr[0, :n - 1, 3]
     else:
