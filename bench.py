@@ -245,6 +245,16 @@ def main():
     launches_per_step = eng.launches()
     N = L // 64
     selected = int(eng.sel.counts.to(torch.int64).sum().item())
+    # tile efficiency of attn_kernel: each M=128 tile (two 64-row query groups that
+    # share a KV head) issues S / P.V for the UNION of its groups' selections
+    tile_eff = None
+    if G % 4 == 0 and len(heads) % 4 == 0:
+        dm = eng.sel.dense_mask()[0]                                   # [H, N, N] bool
+        pairs = dm.view(len(heads) // 2, 2, N, N)
+        union = (pairs[:, 0] | pairs[:, 1]).sum().item()
+        tile_eff = {"useful_group_steps": selected, "issued_tile_steps": int(union),
+                    "rows_useful_fraction": selected / (2.0 * union)}
+        del dm, pairs
     causal = len(heads) * N * (N + 1) // 2
     rho = 1.0 - selected / causal
 
@@ -375,7 +385,7 @@ def main():
                gpu_launches=launches_per_step * args.steps,
                roofline=roof, cpu_baseline=cpu,
                stages_ms=stage_ms, stage_roofline=stage_roofs,
-               sparsity={"rho": rho, "selected_blocks": selected, "causal_blocks": causal},
+               sparsity={"rho": rho, "selected_blocks": selected, "causal_blocks": causal, "attn_tiles": tile_eff},
                dense_baselines_ms=dense, verify_gather=gather,
                speedup_vs_dense={"vs": fastest[0], "dense_ms": fastest[1], "speedup": fastest[1] / ms} if fastest else None)
     print(json.dumps(out), flush=True)

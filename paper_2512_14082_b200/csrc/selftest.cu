@@ -317,6 +317,17 @@ __global__ void ex2_rate_kernel(int iters, int mode, float* sink, long long* cyc
         v[c] = p.x - 1.0f;
         v[c + 1] = p.y - 1.0f;
       }
+    } else if (mode == 3) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        // packed half-precision exp2: one MUFU op for two results (if the pipe allows)
+        __half2 h = __floats2half2_rn(v[c], v[c + 1]);
+        uint32_t hb = *reinterpret_cast<uint32_t*>(&h), rb;
+        asm("ex2.approx.f16x2 %0, %1;" : "=r"(rb) : "r"(hb));
+        const float2 r = __half22float2(*reinterpret_cast<__half2*>(&rb));
+        v[c] = r.x - 1.0f;
+        v[c + 1] = r.y - 1.0f;
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < 32; c += 2) {

@@ -9,7 +9,7 @@ st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 for threads in (128, 256, 512):
     out = torch.zeros(148, dtype=torch.int64, device="cuda")
     sink = torch.zeros(148 * threads, dtype=torch.float32, device="cuda")
-    for mode, name in ((0, "MUFU ex2"), (1, "poly ex2"), (2, "FFMA2")):
+    for mode, name in ((0, "MUFU ex2"), (1, "poly ex2"), (2, "FFMA2"), (3, "ex2 f16x2")):
         iters = 2000
         L.us_selftest_ex2_rate(iters, mode, 148, threads, C.c_void_p(sink.data_ptr()), C.c_void_p(out.data_ptr()), st)
         torch.cuda.synchronize()
