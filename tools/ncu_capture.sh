@@ -15,7 +15,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
 # 2. full sets: attention (dominant), proxy passes 1+2, compress/split/select
 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 1 -c 1 \
     -o gpurun_out/ncu_${TAG}_attn python tools/profile_case.py $L $H $HKV $GAIN $P > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:proxy_kernel -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:proxy -s 2 -c 2 \
     -o gpurun_out/ncu_${TAG}_proxy python tools/profile_case.py $L $H $HKV $GAIN $P > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'compress_kernel|split_kernel|select_kernel' -s 5 -c 5 \
     -o gpurun_out/ncu_${TAG}_small python tools/profile_case.py $L $H $HKV $GAIN $P > /dev/null 2>&1
