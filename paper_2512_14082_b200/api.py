@@ -374,6 +374,79 @@ class Engine:
     def launches(self) -> int:
         return int(lib().us_last_launch_count())
 
+    # -------------------------------------------------------------- host-buffer path
+    def _chunk_plan(self, chunks: int):
+        """Split the layer into `chunks` runs of whole KV heads (batch 1): every
+        chunk is an independent layer of G*n Q heads over n KV heads (heads never
+        couple), so the chunked result equals the one-call result."""
+        p = self.p
+        G = p.H // p.H_kv
+        if p.B != 1 or p.c_h > G or G % p.c_h:
+            return None
+        chunks = max(1, min(chunks, p.H_kv))
+        sizes = [p.H_kv // chunks + (1 if c < p.H_kv % chunks else 0) for c in range(chunks)]
+        plan, kv0 = [], 0
+        N = p.L // p.S
+        W = (N + 31) // 32
+        for n in sizes:
+            cp = UsParams(1, n * G, n, p.L, p.d_k, p.S, p.c_q, p.c_k, p.c_h, p.strategy, p.causal_mode,
+                          p.select_mode, p.P, p.top_k, p.flags, p.seed)
+            q0, q1 = kv0 * G, (kv0 + n) * G
+            pl0, pl1 = q0 // p.c_h, q1 // p.c_h
+            sel = UsSelection(self.sel.mask_bits[0, pl0:pl1].data_ptr(), self.sel.counts[0, pl0:pl1].data_ptr(),
+                              self.sel.coverage[0, pl0:pl1].data_ptr(), None, None)
+            plan.append((cp, (q0, q1), (kv0, kv0 + n), sel))
+            kv0 += n
+        return plan
+
+    def run_host(self, Qh, Kh, Vh, Oh, chunks: int = 4):
+        """unisparse_attn from (pinned) host buffers: H2D of Q/K/V, the hot path,
+        D2H of O, pipelined over KV-head chunks on three CUDA streams (copy-in,
+        compute, copy-out) so the PCIe transfers overlap the kernels. Enqueues
+        only; returns the event recorded after the last D2H on the copy-out stream."""
+        plan = self._chunk_plan(chunks) if chunks > 1 else None
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_streams"):
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+        s_in, s_comp, s_out = self._streams
+        start = torch.cuda.Event()
+        start.record(cur)
+        for s_ in self._streams:
+            s_.wait_event(start)
+        if plan is None:
+            with torch.cuda.stream(s_comp):
+                self.Q.copy_(Qh, non_blocking=True)
+                self.K.copy_(Kh, non_blocking=True)
+                self.V.copy_(Vh, non_blocking=True)
+                self.run()
+                Oh.copy_(self.O, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(s_comp)
+            cur.wait_event(done)
+            return done
+        G = self.p.H // self.p.H_kv
+        ws = _ptr(self.ws)
+        for cp, (q0, q1), (k0, k1), sel in plan:
+            e_in, e_comp = torch.cuda.Event(), torch.cuda.Event()
+            with torch.cuda.stream(s_in):
+                self.Q[:, q0:q1].copy_(Qh[:, q0:q1], non_blocking=True)
+                self.K[:, k0:k1].copy_(Kh[:, k0:k1], non_blocking=True)
+                self.V[:, k0:k1].copy_(Vh[:, k0:k1], non_blocking=True)
+                e_in.record(s_in)
+            s_comp.wait_event(e_in)
+            _raise(lib().us_unisparse_attention(
+                C.byref(cp), _ptr(self.Q[:, q0:q1]), _ptr(self.K[:, k0:k1]), _ptr(self.V[:, k0:k1]),
+                _ptr(self.O[:, q0:q1]), _ptr(self.lse[:, q0:q1]), C.byref(sel), ws, self.ws.numel(),
+                C.c_void_p(s_comp.cuda_stream)))
+            e_comp.record(s_comp)
+            s_out.wait_event(e_comp)
+            with torch.cuda.stream(s_out):
+                Oh[:, q0:q1].copy_(self.O[:, q0:q1], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(s_out)
+        cur.wait_event(done)
+        return done
+
 
 def selftest_umma(mode: int, N: int, bf16: bool, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     D = torch.empty((128, N), dtype=torch.float32, device=A.device)
