@@ -355,16 +355,21 @@ def main():
     hbm, tf_burst, tf_sust, peak_src = peaks()
     flops_attn = selected * 4 * 64 * 64 * d
     dominant = max(stage_ms.items(), key=lambda kv: kv[1])[0]
+    issued_attn = (tile_eff["issued_tile_steps"] * 2 * 64 * 64 * 4 * d) if tile_eff else None
     if dominant == "attention":
         achieved = flops_attn / (stage_ms["attention"] * 1e-3) / 1e12
         roof = {"kernel": "attn_kernel (tcgen05 block-sparse FA)", "bound": "tensor", "achieved": achieved,
-                "peak": tf_sust, "unit": "TFLOP/s", "frac": achieved / tf_sust}
+                "peak": tf_sust, "unit": "TFLOP/s", "frac": achieved / tf_sust,
+                "algorithmic": "selected_blocks * 4 * S^2 * d (metrics.cpp:83-85)",
+                "issued_tflops": issued_attn / (stage_ms["attention"] * 1e-3) / 1e12 if issued_attn else None}
     else:
         Lq = L // 8
-        fl = 3 * 2 * Lq * Lq * len(heads) * d * 1.5  # fp16x3, post-softmax: full-square lse pass + causal pass
+        fl = 2 * Lq * Lq * len(heads) * d  # compressed_qk (metrics.cpp:60), post-softmax full square
         achieved = fl / (stage_ms["proxy"] * 1e-3) / 1e12
         roof = {"kernel": "proxy_kernel (tcgen05 fp16x3)", "bound": "tensor", "achieved": achieved, "peak": tf_sust,
-                "unit": "TFLOP/s", "frac": achieved / tf_sust}
+                "unit": "TFLOP/s", "frac": achieved / tf_sust,
+                "algorithmic": "compressed_qk = 2 (L/c_q)(L/c_k)(H/c_h) d (metrics.cpp:60)",
+                "issued_tflops": 3 * achieved}
     roof["traffic"] = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
