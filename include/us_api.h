@@ -156,6 +156,12 @@ us_status us_check_device_errors(const us_params* p, void* workspace, void* stre
  * softmax_aggregation, top_p, sparse_attention (0), dense_attention. */
 us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, uint64_t* out6);
 
+/* Block-sparse attention kernel used by every call in this process:
+ * 1 = attention.cu (two M=128 tiles per CTA, 64-key steps; default),
+ * 2 = attention2.cu (one tile per CTA, 128-key steps). Both compute the same
+ * function; the environment variable US_ATTN_IMPL sets the initial choice. */
+us_status us_set_attention_impl(int32_t impl);
+
 /* Number of kernel launches the last successful call on this thread issued. */
 int32_t us_last_launch_count(void);
 

@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -286,6 +288,19 @@ us_status run_select_rows(const us_params& p, const float* scores, int planes, u
   return launch_select(sa, st);
 }
 
+// Attention kernel selection (calibration knob): US_ATTN_IMPL=1 -> attention.cu
+// (64-key steps, two tiles per CTA), 2 -> attention2.cu (128-key steps).
+std::atomic<int> g_attn_impl{-1};
+int attention_impl() {
+  int v = g_attn_impl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = std::getenv("US_ATTN_IMPL");
+    v = (e && std::atoi(e) == 2) ? 2 : 1;
+    g_attn_impl.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
                         const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st) {
   Geo g(p);
@@ -310,6 +325,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.O = static_cast<__nv_bfloat16*>(O);
   a.lse = lse;
   a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  if (attention_impl() == 2) return launch_attention2(a, tK, tV, st);
   return launch_attention(a, tQ, tK, tV, st);
 }
 
@@ -386,6 +402,15 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
   all.insert(all.end(), c.unsupported.begin(), c.unsupported.end());
   if (msg && cap) std::snprintf(msg, cap, "%s", joined(all).c_str());
   return int(all.size());
+}
+
+us_status us_set_attention_impl(int32_t impl) {
+  if (impl != 1 && impl != 2) {
+    set_error("us_set_attention_impl: impl must be 1 (64-key steps) or 2 (128-key steps)");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  g_attn_impl.store(impl, std::memory_order_relaxed);
+  return US_OK;
 }
 
 us_status us_check_params(const us_params* p, const char* who, int32_t need_compression) {

@@ -99,6 +99,11 @@ struct AttnArgs {
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);
 
+// 128-key-step variant (attention2.cu): one M=128 tile per CTA, two union blocks
+// per step; Q is read from global memory by the softmax warps (no Q tensor map).
+us_status launch_attention2(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                            cudaStream_t st);
+
 // mask validation: err |= 4 for a non-causal bit, 8 for an empty causal row;
 // first offending row index (b*planes+p)*N+i recorded with atomicMin in *first_bad.
 us_status launch_mask_check(const uint32_t* mask, int rows, int N, int W, uint32_t* err,

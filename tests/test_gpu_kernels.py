@@ -218,3 +218,34 @@ def test_sparse_attention_rejects_malformed_masks():
     with pytest.raises(ValueError, match="non-causal"):
         us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V),
                                     torch.from_numpy(_bits_from_mask(m)).cuda())
+
+
+@pytest.mark.parametrize("H,H_kv,d", [(8, 4, 128), (4, 4, 64), (6, 2, 128), (3, 1, 128)])
+def test_attention_impls_agree(H, H_kv, d):
+    """attention.cu (64-key steps, two tiles per CTA) and attention2.cu (128-key
+    steps, one tile per CTA) on the same random masks — odd union lengths
+    included: both equal the fp64 oracle within the bf16 tolerance."""
+    import ctypes
+    rng = np.random.default_rng(H * 100 + d)
+    B, L = 2, 1024
+    N = L // 64
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    mask = rng.random((B, H, N, N)) < 0.4
+    mask &= np.tril(np.ones((N, N), bool))
+    mask[..., np.arange(N), np.arange(N)] = True
+    bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
+    lib = us().api.lib()
+    lib.us_set_attention_impl.argtypes = [ctypes.c_int32]
+    try:
+        for impl in (2, 1):
+            assert lib.us_set_attention_impl(impl) == 0
+            Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
+            Og = Og.float().cpu().numpy()
+            lseg = lseg.cpu().numpy()
+            for b in range(B):
+                Or, lser = O.block_sparse_attention(Q[b], K[b], V[b], mask[b], 64)
+                assert np.abs(Og[b] - Or).max() <= ATOL, (impl, b)
+                assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO, (impl, b)
+                assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
+    finally:
+        lib.us_set_attention_impl(1)
