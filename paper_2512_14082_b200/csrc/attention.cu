@@ -106,9 +106,6 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-#ifndef US_ATTN_TURNS
-#define US_ATTN_TURNS 0
-#endif
 #ifndef US_ATTN_POLY_FROM
 #define US_ATTN_POLY_FROM 56
 #endif
@@ -390,33 +387,12 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_q[x]);
     }
-#if US_ATTN_TURNS
-    // The two tiles' exponential phases take turns on the SM's MUFU/FMA pipes in
-    // the total order (union position t, tile A before tile B) — the order the
-    // producer and both issuers follow, so it cannot deadlock. When consecutive
-    // events of that order belong to different tiles, the earlier tile's 128
-    // softmax threads bar.arrive and the later tile's bar.sync on a 256-thread
-    // named barrier (id 1: A -> B, id 2: B -> A; handoffs alternate direction, so
-    // a barrier instance is never arrived on twice). bar.sync blocks in hardware.
-    auto partA = [&](int tt) { return ((steps[tt] >> 16) & 3u) != 0u; };
-    auto partB = [&](int tt) { return ((steps[tt] >> 18) & 3u) != 0u; };
-#endif
     int k = 0;
     for (int t = 0; t < T; ++t) {
       const uint32_t e = steps[t];
       if (((e >> (16 + 2 * x)) & 3u) == 0u) continue;  // not a step of this tile
       const int j = int(e & 0xFFFFu);
       const bool sel = (e >> (16 + g)) & 1u;
-#if US_ATTN_TURNS
-      bool wait_turn, pass_turn;
-      if (x == 0) {
-        wait_turn = t > 0 && partB(t - 1);
-        pass_turn = partB(t) || (t + 1 < T && !partA(t + 1));
-      } else {
-        wait_turn = partA(t) || (t > 0 && !partB(t - 1));
-        pass_turn = t + 1 < T && partA(t + 1);
-      }
-#endif
       mbar_wait(&bar_sfull[x], k & 1);
       tc_fence_after();
       if (row == 0) TRACE(x, k, 1);
@@ -437,9 +413,6 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0) mbar_arrive(&bar_sfree[x]);  // S(k+1) may now overwrite the S columns
       if (row == 0) TRACE(x, k, 4);
       bool pv_prev_done = (k == 0);
-#if US_ATTN_TURNS
-      if (wait_turn) named_bar_sync(x == 0 ? 2 : 1, 256);
-#endif
       uint32_t packed[kBS / 2];
       if (sel) {
         const bool diag = (j == ig);
@@ -519,9 +492,6 @@ __global__ void __launch_bounds__(384, 1)
         for (int c = 0; c < kBS / 2; ++c) packed[c] = 0u;
       }
       if (row == 0) TRACE(x, k, 5);
-#if US_ATTN_TURNS
-      if (pass_turn) named_bar_arrive(x == 0 ? 1 : 2, 256);
-#endif
       // P(k) -> the SWIZZLE_128B P tile (row = 128 B = 8 chunks of 16 B); P.V(k-1)
       // must have consumed P(k-1) first
       if (!pv_prev_done) mbar_wait(&bar_pvdone[x], (k - 1) & 1);
