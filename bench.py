@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense baselines")
     ap.add_argument("--seed", type=int, default=2512)
     ap.add_argument("--flashinfer", action="store_true", help="also time flashinfer dense prefill")
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (nccl; gloo for checks)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="KV-head chunks of the pipelined host-buffer path")
     args = ap.parse_args()
 
@@ -214,8 +215,9 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
+        dist.init_process_group(args.dist_backend, init_method="env://")
+    # (modulo: lets a functional multi-rank check share one GPU; one GPU per rank in production)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     from paper_2512_14082_b200.shard import gather_heads, imbalance, shard_heads
     shards = shard_heads(H, H_kv, world)
     shard = shards[rank]
@@ -234,7 +236,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if args.dist_backend == "gloo" else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -311,10 +313,11 @@ def main():
     gather = None
     if dist:
         t0 = time.perf_counter()
-        full = gather_heads(eng.O, shards)
+        O_loc = eng.O.cpu() if args.dist_backend == "gloo" else eng.O
+        full = gather_heads(O_loc, shards)
         torch.cuda.synchronize()
         sl = full[:, shard.q_heads.start:shard.q_heads.stop]
-        gather = {"backend": dist.get_backend(), "ok": bool(torch.equal(sl, eng.O)),
+        gather = {"backend": dist.get_backend(), "ok": bool(torch.equal(sl, O_loc)),
                   "bytes": full.numel() * full.element_size(), "s": time.perf_counter() - t0,
                   "head_imbalance": imbalance(shards)}
         del full, sl
