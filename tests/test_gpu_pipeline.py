@@ -49,6 +49,9 @@ CASES = [
     (4096, 8, 2, 128, 0.90, O.POST_SOFTMAX, 2, 14),
     (2048, 4, 4, 64, 0.95, O.POST_SOFTMAX, 1, 15),
     (8192, 4, 1, 128, 0.95, O.POST_SOFTMAX, 1, 16),
+    (4096, 7, 1, 128, 0.95, O.POST_SOFTMAX, 1, 17),   # Qwen-like odd GQA group (G = 7)
+    (2048, 4, 4, 64, 0.9, O.POST_SOFTMAX, 2, 18),     # MHA with c_h = 2 (K pooled per compressed head)
+    (4096, 8, 2, 128, 0.95, O.PRE_SOFTMAX, 2, 19),    # pre-softmax with head compression
 ]
 
 
