@@ -356,3 +356,86 @@ extern "C" us_status us_selftest_ex2_rate(int iters, int mode, int ctas, int thr
   US_LAUNCH_CHECK("us_selftest_ex2_rate");
   return US_OK;
 }
+
+// ---------------------------------------------------------------- softmax-step probe
+// The exponential phase of one attention step (attention.cu, 64 key columns per
+// thread: row max, FFMA2 scale, 56 MUFU ex2 + 4 cubic pairs, FADD2 row sum, bf16
+// pack) on register data, `iters` times back to back, one warp per SMSP (128
+// threads) or more. Output: cycles per CTA. Isolates the instruction mix from the
+// kernel's TMEM / barrier traffic.
+namespace us {
+namespace {
+__device__ __forceinline__ float2 probe_poly2b(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
+  float2 p = __ffma2_rn(make_float2(0.0551f, 0.0551f), f, make_float2(0.2426f, 0.2426f));
+  p = __ffma2_rn(p, f, make_float2(0.6933f, 0.6933f));
+  p = __ffma2_rn(p, f, make_float2(0.9999f, 0.9999f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+__global__ void softmax_probe_kernel(int iters, int mode, uint32_t* sink, long long* cycles_out) {
+  // mode bits: 1 = F2FP bf16 packing, 2 = FADD2 row-sum, 4 = row max, 8 = 12.5 % cubic exp2
+  float sv[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) sv[c] = 0.01f * float((threadIdx.x * 7 + c * 13) & 63);
+  float m_used = 0.f, l = 0.f;
+  uint32_t acc_bits = 0;
+  const float sl2 = 0.1275f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    if (mode & 4) {
+      float m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = fmaxf(sv[u], fmaxf(sv[8 + u], sv[16 + u]));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(sv[24 + u], sv[32 + u]));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = fmaxf(m8[u], fmaxf(sv[40 + u], fmaxf(sv[48 + u], sv[56 + u])));
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * sl2;
+      if (mx > m_used + 8.f) m_used = mx;
+    }
+    const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
+    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    uint32_t packed[32];
+#pragma unroll
+    for (int c = 0; c < 64; c += 2) {
+      const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+      float2 p;
+      if ((mode & 8) && c >= 56) {
+        p = probe_poly2b(xx);
+      } else {
+        p.x = ex2_approx(xx.x);
+        p.y = ex2_approx(xx.y);
+      }
+      if (mode & 2) acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
+      packed[c >> 1] = (mode & 1) ? pack_bf16(p.x, p.y) : (__float_as_uint(p.x) ^ __float_as_uint(p.y));
+    }
+    const float2 s2 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+    l += s2.x + s2.y;
+#pragma unroll
+    for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+      for (int c = 0; c < w; ++c) packed[c] ^= packed[c + w];
+    acc_bits ^= packed[0];
+    m_used += 1e-7f;
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc_bits ^ __float_as_uint(l);
+  if (threadIdx.x == 0) cycles_out[blockIdx.x] = t1 - t0;
+}
+}  // namespace
+}  // namespace us
+
+extern "C" us_status us_selftest_softmax_probe(int iters, int mode, int ctas, int threads, uint32_t* sink,
+                                               long long* cycles_out, void* stream) {
+  using namespace us;
+  softmax_probe_kernel<<<ctas, threads, 0, static_cast<cudaStream_t>(stream)>>>(iters, mode, sink, cycles_out);
+  US_LAUNCH_CHECK("us_selftest_softmax_probe");
+  return US_OK;
+}
