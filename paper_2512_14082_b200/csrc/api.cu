@@ -90,7 +90,8 @@ Checked check(const us_params& p, bool need_compression) {
   if (p.L / std::max(p.S, 1) > 4096) u.push_back("N=L/S above 4096 unsupported on the GPU path");
   if ((long long)p.B * p.H * p.L >= (1ll << 31)) u.push_back("B*H*L must stay below 2^31 rows");
   if (need_compression) {
-    if (p.strategy != US_POOL_MEAN) u.push_back("only mean pooling is implemented on the GPU path");
+    if (p.strategy != US_POOL_MEAN && p.strategy != US_POOL_MAX && p.strategy != US_POOL_STOCHASTIC)
+      u.push_back("unknown pooling strategy");
     if (!is_pow2(p.S / p.c_q) || !is_pow2(p.S / p.c_k))
       u.push_back("S/c_q and S/c_k must be powers of two on the GPU path");
   }
@@ -141,7 +142,9 @@ struct Geo {
     Lk = L / p.c_k;
     rq = S / p.c_q;
     rk = S / p.c_k;
-    kv_dedup = (G % p.c_h) == 0;
+    // one pooled K per KV head when the expanded copies are identical: every strategy
+    // but stochastic (whose per-head seeds differ, compression.cpp:19-20)
+    kv_dedup = (G % p.c_h) == 0 && p.strategy != US_POOL_STOCHASTIC;
     kv_planes = kv_dedup ? H_kv : Hc;
     kv_mul = kv_dedup ? p.c_h : 1;
     kv_div = kv_dedup ? G : 1;
@@ -218,12 +221,12 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   Ws w = layout(p);
   US_CUDA_TRY(cudaMemsetAsync(ws, 0, w.header_bytes, st), "workspace clear");
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p.c_q, g.Hc, p.c_h, 1,
-                  at<float>(ws, w.qc), at<uint32_t>(ws, w.absmax_q)};
+                  at<float>(ws, w.qc), at<uint32_t>(ws, w.absmax_q), p.strategy, 0, p.seed};
   us_status s = launch_compress(cq, st);
   if (s != US_OK) return s;
   CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p.c_k, g.kv_planes,
                   g.kv_dedup ? 1 : p.c_h, g.kv_dedup ? 1 : g.G, at<float>(ws, w.kc),
-                  at<uint32_t>(ws, w.absmax_k)};
+                  at<uint32_t>(ws, w.absmax_k), p.strategy, 1, p.seed};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
   SplitArgs sq{at<float>(ws, w.qc), g.B * g.Hc, g.Lq, g.D, at<uint32_t>(ws, w.absmax_q),
                at<int>(ws, w.exp_q), at<__half>(ws, w.qh), at<__half>(ws, w.ql)};
@@ -431,9 +434,11 @@ us_status us_compress(const us_params* p, const void* Q, const void* K, float* Q
   Geo g(*p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // reference layout: H/c_h planes for both Q and K (K expanded to H heads first)
-  CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p->c_q, g.Hc, p->c_h, 1, Qc, nullptr};
+  CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p->c_q, g.Hc, p->c_h, 1, Qc, nullptr,
+                  p->strategy, 0, p->seed};
   if ((s = launch_compress(cq, st)) != US_OK) return s;
-  CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p->c_k, g.Hc, p->c_h, g.G, Kc, nullptr};
+  CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p->c_k, g.Hc, p->c_h, g.G, Kc, nullptr,
+                  p->strategy, 1, p->seed};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "compress");
   return US_OK;

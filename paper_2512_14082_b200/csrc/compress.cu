@@ -43,17 +43,37 @@ __device__ __forceinline__ double divide(double x, double div, double inv) {
   return inv != 0.0 ? x * inv : x / div;
 }
 
+// SplitMix64 counter RNG and seed chaining of the reference (rng.hpp:11-67).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+__device__ __forceinline__ uint64_t chain_seed(uint64_t s, uint64_t tag) { return mix64(s + kGamma + tag); }
+
+// Sum over the `width` consecutive lanes that share one output row, reduced to
+// the group's first lane in a fixed tree and broadcast, so every lane of the
+// group holds the identical value.
+__device__ __forceinline__ double group_sum(double v, int width) {
+  for (int o = width >> 1; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, width);
+  return __shfl_sync(0xffffffffu, v, 0, width);
+}
+
 __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
   const int chunks = a.d / 8;
   const int Lc = a.L / a.c;
   const long long total = (long long)a.B * a.planes * Lc * chunks;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = tid < total;
+  // inactive lanes mirror the last row: the stochastic path shuffles across the
+  // lanes of a row group, so every lane of a warp runs it
+  const long long tid_eff = active ? tid : total - chunks + tid % chunks;
   float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int plane_id = 0;
-  if (active) {
-    const int ch = int(tid % chunks);
-    long long r = tid / chunks;
+  {
+    const int ch = int(tid_eff % chunks);
+    long long r = tid_eff / chunks;
     const int t = int(r % Lc);
     r /= Lc;
     const int p = int(r % a.planes);
@@ -61,45 +81,111 @@ __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double in
     plane_id = b * a.planes + p;
     double hacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int g = 0; g < a.members; ++g) {
-      const int hs = (p * a.members + g) / a.div;
+      const int h = p * a.members + g;  // head index in the reference's (expanded) numbering
+      const int hs = h / a.div;
       const uint4* src = reinterpret_cast<const uint4*>(
           a.src + (((long long)b * a.H_src + hs) * a.L + (long long)t * a.c) * a.d + ch * 8);
       const int stride = a.d / 8;  // uint4 per row
-      double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      int rr = 0;
-      for (; rr + 8 <= a.c; rr += 8) {
-        uint4 v[8];
+      float val[8];
+      if (a.strategy == US_POOL_MEAN || a.c == 1) {
+        // (c == 1 returns the window row unchanged for every strategy, compression.hpp:20)
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int rr = 0;
+        for (; rr + 8 <= a.c; rr += 8) {
+          uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = ld_stream(src + (rr + u) * stride);
+          for (int u = 0; u < 8; ++u) v[u] = ld_stream(src + (rr + u) * stride);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) bf16x8_to_f64_add(v[u], acc);
+          for (int u = 0; u < 8; ++u) bf16x8_to_f64_add(v[u], acc);
+        }
+        for (; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) val[e] = __double2float_rn(divide(acc[e], double(a.c), inv_c));
+      } else if (a.strategy == US_POOL_MAX) {
+        // column max over the window (compression.hpp:30-32); exact
+#pragma unroll
+        for (int e = 0; e < 8; ++e) val[e] = -INFINITY;
+        for (int rr = 0; rr < a.c; ++rr) {
+          const uint4 v = ld_stream(src + rr * stride);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            val[2 * q] = fmaxf(val[2 * q], __uint_as_float(w[q] << 16));
+            val[2 * q + 1] = fmaxf(val[2 * q + 1], __uint_as_float(w[q] & 0xFFFF0000u));
+          }
+        }
+      } else {
+        // stochastic (compression.hpp:33-53): pick window row r with probability
+        // |row r| / sum of row norms, drawn from CounterRng(chain(chain(seed, role, h), t)).
+        // Row norms: fp64 sums of squares (exact for bf16 inputs), sqrt, summed in row order.
+        uint64_t state = chain_seed(chain_seed(chain_seed(a.seed, uint64_t(a.role)), uint64_t(h)), uint64_t(t));
+        auto row_norm = [&](int rr) {
+          const uint4 v = ld_stream(src + rr * stride);
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          double s2 = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double lo = double(__uint_as_float(w[q] << 16)), hi = double(__uint_as_float(w[q] & 0xFFFF0000u));
+            s2 += lo * lo;
+            s2 += hi * hi;
+          }
+          return sqrt(group_sum(s2, chunks));
+        };
+        double tot = 0.0;
+        for (int rr = 0; rr < a.c; ++rr) tot += row_norm(rr);
+        int pick = a.c - 1;
+        state += kGamma;
+        const uint64_t draw = mix64(state);
+        if (tot > 0.0) {
+          const double u = double(draw >> 11) * 0x1.0p-53 * tot;
+          double cum = 0.0;
+          bool found = false;
+          for (int rr = 0; rr < a.c; ++rr) {  // fixed trip count: shuffles stay warp-uniform
+            cum += row_norm(rr);
+            if (!found && u < cum) {
+              pick = rr;
+              found = true;
+            }
+          }
+        } else {
+          pick = int(draw % uint64_t(a.c));
+        }
+        const uint4 v = ld_stream(src + pick * stride);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          val[2 * q] = __uint_as_float(w[q] << 16);
+          val[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+        }
       }
-      for (; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
       if (a.members == 1) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) res[e] = __double2float_rn(divide(acc[e], double(a.c), inv_c));
+        for (int e = 0; e < 8; ++e) res[e] = val[e];
       } else {
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          hacc[e] += double(__double2float_rn(divide(acc[e], double(a.c), inv_c)));
+        for (int e = 0; e < 8; ++e) hacc[e] += double(val[e]);
       }
     }
     if (a.members > 1) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) res[e] = __double2float_rn(divide(hacc[e], double(a.members), inv_m));
     }
-    float4* dst = reinterpret_cast<float4*>(a.out + (((long long)plane_id) * Lc + t) * a.d + ch * 8);
-    dst[0] = make_float4(res[0], res[1], res[2], res[3]);
-    dst[1] = make_float4(res[4], res[5], res[6], res[7]);
+    if (active) {
+      float4* dst = reinterpret_cast<float4*>(a.out + (((long long)plane_id) * Lc + t) * a.d + ch * 8);
+      dst[0] = make_float4(res[0], res[1], res[2], res[3]);
+      dst[1] = make_float4(res[4], res[5], res[6], res[7]);
+    }
   }
   if (a.absmax) {
     float m = 0.f;
+    if (active) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(res[e]));
-    // NaN sorts above every finite value as unsigned bits; keep it visible.
+      for (int e = 0; e < 8; ++e) m = fmaxf(m, fabsf(res[e]));
+      // NaN sorts above every finite value as unsigned bits; keep it visible.
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      if (res[e] != res[e]) m = __uint_as_float(0x7FC00000u);
+      for (int e = 0; e < 8; ++e)
+        if (res[e] != res[e]) m = __uint_as_float(0x7FC00000u);
+    }
     const unsigned full = __activemask();
     const int leader_plane = __shfl_sync(full, plane_id, 0);
     const bool uniform = __all_sync(full, !active || plane_id == leader_plane);

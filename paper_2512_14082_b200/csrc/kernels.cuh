@@ -27,6 +27,9 @@ struct CompressArgs {
   int div;         // member head -> source head divisor (G for expanded K, 1 for Q)
   float* out;      // f32 [B][planes][L/c][d]
   uint32_t* absmax;  // [B * planes] max |out| as f32 bits (may be null)
+  int strategy;    // US_POOL_MEAN / MAX / STOCHASTIC (compression.hpp:24-53)
+  int role;        // stochastic seed tag: 0 = Q, 1 = K (compression.cpp:17-20)
+  uint64_t seed;   // CompressionConfig::seed
 };
 us_status launch_compress(const CompressArgs& a, cudaStream_t st);
 

@@ -61,6 +61,28 @@ def test_compress_bit_exact(c_q, c_k, c_h, H, H_kv):
         assert (Kc[b].view(np.uint32) == rk.view(np.uint32)).all()
 
 
+@pytest.mark.parametrize("strategy", [1, 2])  # POOL_MAX, POOL_STOCHASTIC
+@pytest.mark.parametrize("c_q,c_k,c_h,H,H_kv", [(8, 8, 1, 8, 2), (4, 8, 2, 8, 2), (8, 8, 2, 4, 4),
+                                               (64, 16, 1, 4, 1), (1, 2, 1, 2, 2)])
+def test_compress_strategies_bit_exact(strategy, c_q, c_k, c_h, H, H_kv):
+    """Max and stochastic pooling (compression.hpp:30-53; ablations of PAPER.md:629):
+    the stochastic pick uses the reference's SplitMix64 stream chain(chain(seed,
+    role, head), window) and row-norm weights, so the picked rows equal the oracle's."""
+    rng = np.random.default_rng(strategy * 1000 + c_q * 10 + c_h)
+    B, L, d = 2, 512, 128
+    Q = O.bf16_round(rng.standard_normal((B, H, L, d)).astype(np.float32) * 3)
+    K = O.bf16_round(rng.standard_normal((B, H_kv, L, d)).astype(np.float32))
+    Q[0, 0, :64] = 0.0  # all-zero windows: the stochastic rule falls back to next_u64() % c
+    cfg = us().CompressionConfig(c_q=c_q, c_k=c_k, c_h=c_h, strategy=strategy, seed=987654321)
+    Qc, Kc = us().compress(to_dev_bf16(Q), to_dev_bf16(K), cfg)
+    Qc, Kc = Qc.cpu().numpy(), Kc.cpu().numpy()
+    for b in range(B):
+        c = O.cfg(H, L, d, 64, H_kv=H_kv, c_q=c_q, c_k=c_k, c_h=c_h, strategy=strategy, seed=987654321)
+        rq, rk = O.compress(c, Q[b], K[b])
+        assert (Qc[b].view(np.uint32) == rq.view(np.uint32)).all()
+        assert (Kc[b].view(np.uint32) == rk.view(np.uint32)).all()
+
+
 # ------------------------------------------------------------------ selection on given scores
 def _random_planes(rng, planes, N, kind):
     s = rng.random((planes, N, N)).astype(np.float32)

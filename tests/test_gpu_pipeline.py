@@ -25,15 +25,16 @@ def us():
     return m
 
 
-def _run_case(L, H, H_kv, d, P, mode, c_h, seed, gain=8.0, kind=O.WL_PLANTED, c_q=8, c_k=8):
+def _run_case(L, H, H_kv, d, P, mode, c_h, seed, gain=8.0, kind=O.WL_PLANTED, c_q=8, c_k=8, strategy=0):
     Q, K, V, planted = workload(kind, L, H, H_kv, d, seed, gain=gain)
-    cfg = us().CompressionConfig(c_q=c_q, c_k=c_k, c_h=c_h, P=P, causal_mode=mode)
+    cfg = us().CompressionConfig(c_q=c_q, c_k=c_k, c_h=c_h, P=P, causal_mode=mode, strategy=strategy, seed=seed)
     res = us().unisparse_attn(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1), cfg,
                               with_scores=True)
     torch.cuda.synchronize()
     gpu_scores = res.report.mask.scores[0].cpu().numpy()
     gpu_mask = res.report.mask.dense_mask()[0].cpu().numpy()
-    c = O.cfg(H, L, d, 64, H_kv=H_kv, c_q=c_q, c_k=c_k, c_h=c_h, causal_mode=mode, P=P)
+    c = O.cfg(H, L, d, 64, H_kv=H_kv, c_q=c_q, c_k=c_k, c_h=c_h, causal_mode=mode, P=P, strategy=strategy,
+              seed=seed)
     Qc, Kc = O.compress(c, Q, K)
     ref_scores = O.proxy_scores(c, Qc, Kc)
     ref_mask, _ = O.build_block_mask(ref_scores, H, c_h, P)
@@ -190,3 +191,12 @@ def test_run_host_pipelined_equals_device_path():
         torch.cuda.synchronize()
         assert torch.equal(Oh.cuda(), O_ref), chunks
         assert torch.equal(eng.sel.mask_bits, mask_ref), chunks
+
+
+@pytest.mark.parametrize("strategy", [1, 2])
+def test_pooling_ablations_masks_bit_exact(strategy):
+    """Max / stochastic pooling end to end (PAPER.md:629 ablation): masks equal the
+    reference rule on the reference pooling."""
+    r = _run_case(4096, 4, 2, 128, 0.95, O.POST_SOFTMAX, 1, 31 + strategy, strategy=strategy)
+    flips = int((r["gpu_mask"] != r["ref_mask"]).sum())
+    assert flips == 0, flips
