@@ -56,7 +56,8 @@ typedef enum us_status {
   US_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
   US_ERR_INVALID_MASK = 4,     /* non-causal bit or empty row (attention.cpp:106-108,127-129) */
   US_ERR_NONFINITE = 5,        /* negative/NaN proxy scores (selection.cpp:14-15) */
-  US_ERR_WORKSPACE = 6         /* workspace missing or too small */
+  US_ERR_WORKSPACE = 6,        /* workspace missing or too small */
+  US_ERR_IO = 7                /* file I/O: reference std::runtime_error (tensor_io.cpp:15-17) */
 } us_status;
 
 /* PoolStrategy (types.hpp:34) — the GPU path implements Mean. */
@@ -173,6 +174,25 @@ int32_t us_last_launch_count(void);
 us_status us_profile_enable(int32_t max_calls);
 int32_t us_profile_read(float* ms_out, int32_t max_calls);
 void us_profile_disable(void);
+
+/* ---- on-disk formats of the reference (host memory, no CUDA calls) ----------
+ * unisparse.tn tensors (tensor_io.hpp:9-14; write_tensor / read_tensor,
+ * tensor_io.cpp:31-81): 12-byte magic "unisparse.tn", u32 version 1, u32 H, L,
+ * d_k, then H*L*d_k little-endian f32, head major. Errors carry the reference
+ * text ("tensor file <path>: bad magic at offset 0", "payload shorter than
+ * header H*L*d_k at offset ...", "trailing bytes beyond header H*L*d_k"). */
+us_status us_write_tensor(const char* path, const float* data, int32_t H, int32_t L, int32_t d_k);
+us_status us_read_tensor_header(const char* path, int32_t* H, int32_t* L, int32_t* d_k);
+us_status us_read_tensor(const char* path, float* out, size_t capacity_floats);
+
+/* RLE block-mask JSON (save_mask_json / load_mask_json, selection.cpp:90-144),
+ * byte-identical to the reference's nlohmann dump(1, '\t'). mask_bits: host
+ * [H/c_h][N][ceil(N/32)] planes, broadcast to the H heads. us_load_mask_json
+ * fills H, N, P and, when out_bits is non-NULL, per-head bits [H][N][ceil(N/32)]. */
+us_status us_save_mask_json(const char* path, const uint32_t* mask_bits, int32_t H, int32_t N, int32_t c_h,
+                            double P);
+us_status us_load_mask_json(const char* path, int32_t* H, int32_t* N, double* P, uint32_t* out_bits,
+                            size_t capacity_words);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("US_LIB_PATH_OVERRIDE") or os.path.join(_PKG, "_build", "libunisparse_b200.so")
 
 US_OK, US_ERR_INVALID_ARGUMENT, US_ERR_UNSUPPORTED, US_ERR_CUDA, US_ERR_INVALID_MASK, \
-    US_ERR_NONFINITE, US_ERR_WORKSPACE = range(7)
+    US_ERR_NONFINITE, US_ERR_WORKSPACE, US_ERR_IO = range(8)
 POOL_MEAN, POOL_MAX, POOL_STOCHASTIC = 0, 1, 2
 POST_SOFTMAX_BLOCK_CAUSAL, PRE_SOFTMAX_COMPRESSED_CAUSAL = 0, 1
 SELECT_TOP_P, SELECT_TOP_K = 0, 1
@@ -49,6 +49,10 @@ class InvalidMaskError(ValueError):
 
 class CudaError(RuntimeError):
     pass
+
+
+class IoError(RuntimeError):
+    """File I/O failure (the reference throws std::runtime_error, tensor_io.cpp:15-17)."""
 
 
 class UsParams(C.Structure):
@@ -106,6 +110,11 @@ def lib() -> C.CDLL:
             L.us_selection_flops.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp]
             L.us_selftest_umma.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]
             L.us_last_launch_count.restype = C.c_int32
+            L.us_write_tensor.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32]
+            L.us_read_tensor_header.argtypes = [C.c_char_p, vp, vp, vp]
+            L.us_read_tensor.argtypes = [C.c_char_p, vp, C.c_size_t]
+            L.us_save_mask_json.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32, C.c_double]
+            L.us_load_mask_json.argtypes = [C.c_char_p, vp, vp, vp, vp, C.c_size_t]
             L.us_profile_enable.argtypes = [C.c_int32]
             L.us_profile_read.argtypes = [C.c_void_p, C.c_int32]
             L.us_profile_read.restype = C.c_int32
@@ -120,6 +129,8 @@ def _raise(status: int, default: str = ""):
         raise ValueError(msg)
     if status == US_ERR_UNSUPPORTED:
         raise UnsupportedError(msg)
+    if status == US_ERR_IO:
+        raise IoError(msg)
     if status in (US_ERR_INVALID_MASK, US_ERR_NONFINITE):
         raise InvalidMaskError(msg) if status == US_ERR_INVALID_MASK else ValueError(msg)
     raise CudaError(f"status {status}: {msg}")
@@ -471,3 +482,49 @@ def profile_read(max_calls: int):
 
 def profile_disable():
     lib().us_profile_disable()
+
+
+# ------------------------------------------------------------------ on-disk formats (host side)
+def write_tensor(path: str, data) -> None:
+    """write_tensor (tensor_io.cpp:31-47): f32 [H, L, d_k] array-like -> unisparse.tn file."""
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+    if a.ndim != 3:
+        raise ValueError("write_tensor: expected [H, L, d_k]")
+    _raise(lib().us_write_tensor(path.encode(), a.ctypes.data, *a.shape))
+
+
+def read_tensor(path: str):
+    """read_tensor (tensor_io.cpp:49-81) -> numpy f32 [H, L, d_k]."""
+    import numpy as np
+    H, L, d = C.c_int32(), C.c_int32(), C.c_int32()
+    _raise(lib().us_read_tensor_header(path.encode(), C.byref(H), C.byref(L), C.byref(d)))
+    out = np.empty((H.value, L.value, d.value), np.float32)
+    _raise(lib().us_read_tensor(path.encode(), out.ctypes.data, out.size))
+    return out
+
+
+def save_mask_json_bits(path: str, bits, H: int, N: int, c_h: int, P: float) -> None:
+    """save_mask_json (selection.cpp:90-117) from host u32 planes [H/c_h, N, ceil(N/32)]."""
+    import numpy as np
+    b = np.ascontiguousarray(np.asarray(bits).view(np.uint32))
+    if b.shape != (H // c_h, N, (N + 31) // 32):
+        raise ValueError(f"save_mask_json: bits shape {b.shape} != {(H // c_h, N, (N + 31) // 32)}")
+    _raise(lib().us_save_mask_json(path.encode(), b.ctypes.data, H, N, c_h, float(P)))
+
+
+def save_mask_json(path: str, sel: "Selection", H: int, P: float) -> None:
+    """save_mask_json of a Selection (batch item 0)."""
+    save_mask_json_bits(path, sel.mask_bits[0].contiguous().cpu().numpy(), H, sel.N, sel.c_h, P)
+
+
+def load_mask_json(path: str):
+    """load_mask_json (selection.cpp:119-144) -> (bool mask [H, N, N], P)."""
+    import numpy as np
+    H, N, P = C.c_int32(), C.c_int32(), C.c_double()
+    _raise(lib().us_load_mask_json(path.encode(), C.byref(H), C.byref(N), C.byref(P), None, 0))
+    W = (N.value + 31) // 32
+    bits = np.zeros((H.value, N.value, W), np.uint32)
+    _raise(lib().us_load_mask_json(path.encode(), C.byref(H), C.byref(N), C.byref(P), bits.ctypes.data, bits.size))
+    m = ((bits[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(H.value, N.value, W * 32)
+    return m[..., : N.value], P.value
