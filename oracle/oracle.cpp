@@ -424,6 +424,87 @@ int or_proxy_score_rows(const or_cfg* cfg, const float* Qc, const float* Kc, int
   return 0;
 }
 
+// antidiagonal_block_scores (baselines.cpp:10-52): every query t samples the keys
+// s = res, res + stride, ... <= t with res = (S - 1 - t % S) % stride, softmax over
+// those samples, probabilities added to score(t / S, s / S); j > i masked.
+int or_antidiagonal_block_scores(int H, int H_kv, int L, int d, int S, int stride, const float* Q,
+                                 const float* K, double* scores, int nthreads) {
+  if (H <= 0 || L <= 0 || d <= 0 || S <= 0 || L % S || H_kv <= 0 || H % H_kv)
+    return fail("antidiagonal_block_scores: bad dimensions");
+  if (stride <= 0 || S % stride != 0) return fail("antidiagonal_block_scores: stride must divide S");
+  const int N = L / S, G = H / H_kv;
+  const double inv_scale = 1.0 / std::sqrt(double(d));
+  const int nt = nthreads_or_default(nthreads);
+#pragma omp parallel for collapse(2) schedule(dynamic, 1) num_threads(nt)
+  for (int h = 0; h < H; ++h)
+    for (int i = 0; i < N; ++i) {
+      const float* Kh = K + size_t(h / G) * L * d;
+      double* row = scores + (size_t(h) * N + i) * N;
+      for (int j = 0; j < N; ++j) row[j] = j <= i ? 0.0 : kMaskedScore;
+      std::vector<double> logits;
+      for (int q = 0; q < S; ++q) {
+        const int t = i * S + q;
+        const int res = (S - 1 - q) % stride;
+        if (res > t) continue;
+        const int cnt = (t - res) / stride + 1;
+        logits.resize(cnt);
+        const float* qt = Q + (size_t(h) * L + t) * d;
+        double m = -kInf;
+        for (int c = 0; c < cnt; ++c) {
+          logits[c] = dot_f32(qt, Kh + size_t(res + c * stride) * d, d) * inv_scale;
+          m = std::max(m, logits[c]);
+        }
+        double den = 0.0;
+        for (int c = 0; c < cnt; ++c) {
+          logits[c] = std::exp(logits[c] - m);
+          den += logits[c];
+        }
+        for (int c = 0; c < cnt; ++c) row[(res + c * stride) / S] += logits[c] / den;
+      }
+    }
+  return 0;
+}
+
+// last_block_probe_scores (baselines.cpp:54-87): column mass of the last S query
+// rows (causal), replicated to every row's causal prefix.
+int or_last_block_probe_scores(int H, int H_kv, int L, int d, int S, const float* Q, const float* K,
+                               double* scores, int nthreads) {
+  if (H <= 0 || L <= 0 || d <= 0 || S <= 0 || L % S || H_kv <= 0 || H % H_kv)
+    return fail("last_block_probe_scores: bad dimensions");
+  const int N = L / S, G = H / H_kv;
+  const double inv_scale = 1.0 / std::sqrt(double(d));
+  const int nt = nthreads_or_default(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+  for (int h = 0; h < H; ++h) {
+    const float* Kh = K + size_t(h / G) * L * d;
+    std::vector<double> colmass(N, 0.0), row(L);
+    for (int r = 0; r < S; ++r) {
+      const float* qt = Q + (size_t(h) * L + size_t(N - 1) * S + r) * d;
+      const int live = (N - 1) * S + r + 1;
+      double m = -kInf;
+      for (int k = 0; k < live; ++k) {
+        row[k] = dot_f32(qt, Kh + size_t(k) * d, d) * inv_scale;
+        m = std::max(m, row[k]);
+      }
+      double den = 0.0;
+      for (int k = 0; k < live; ++k) {
+        row[k] = std::exp(row[k] - m);
+        den += row[k];
+      }
+      for (int j = 0; j < N; ++j) {
+        const int len = std::min(S, live - j * S);
+        if (len <= 0) continue;
+        double seg = 0.0;
+        for (int k = 0; k < len; ++k) seg += row[j * S + k];
+        colmass[j] += seg / den;
+      }
+    }
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) scores[(size_t(h) * N + i) * N + j] = j <= i ? colmass[j] : kMaskedScore;
+  }
+  return 0;
+}
+
 // top_p_row (selection.cpp:11-48)
 int or_top_p_row(const double* scores, int n, double P, int32_t* indices, int* count,
                  double* covered) {

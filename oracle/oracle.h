@@ -23,6 +23,7 @@
  *   compress            src/compression.cpp:5-25
  *   compressed_attention src/proxy.cpp:10-46
  *   block_aggregate     src/proxy.cpp:48-72
+ *   antidiagonal_block_scores, last_block_probe_scores  src/baselines.cpp:10-87
  *   top_p_row           src/selection.cpp:11-48
  *   build_block_mask    src/selection.cpp:60-88
  *   dense_attention     src/attention.cpp:20-54
@@ -89,6 +90,12 @@ int or_proxy_scores(const or_cfg* cfg, const float* Qc, const float* Kc, double*
  * out[r][N] for qblocks[r]. Cost O(rows * L/c_k * d): used for spot checks. */
 int or_proxy_score_rows(const or_cfg* cfg, const float* Qc, const float* Kc, int hc,
                         const int32_t* qblocks, int nrows, double* out, int nthreads);
+
+/* --- competitor proxies (baselines.cpp:10-87), H planes [H][N][N], j > i = kMaskedScore --- */
+int or_antidiagonal_block_scores(int H, int H_kv, int L, int d_k, int S, int stride, const float* Q,
+                                 const float* K, double* scores, int nthreads);
+int or_last_block_probe_scores(int H, int H_kv, int L, int d_k, int S, const float* Q, const float* K,
+                               double* scores, int nthreads);
 
 /* --- selection --- */
 int or_top_p_row(const double* scores, int n, double P, int32_t* indices, int* count,

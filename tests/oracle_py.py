@@ -161,6 +161,25 @@ def proxy_score_rows(c: OrCfg, Qc, Kc, hc: int, qblocks, nthreads=0):
     return out
 
 
+# ---------------------------------------------------------------- competitor proxies
+def antidiagonal_block_scores(Q, K, S: int, stride: int, nthreads=0):
+    H, L, d = Q.shape
+    N = L // S
+    out = np.zeros((H, N, N), np.float64)
+    _check(lib().or_antidiagonal_block_scores(H, K.shape[0], L, d, S, stride, _p(np.ascontiguousarray(Q, np.float32)),
+                                              _p(np.ascontiguousarray(K, np.float32)), _p(out), nthreads))
+    return out
+
+
+def last_block_probe_scores(Q, K, S: int, nthreads=0):
+    H, L, d = Q.shape
+    N = L // S
+    out = np.zeros((H, N, N), np.float64)
+    _check(lib().or_last_block_probe_scores(H, K.shape[0], L, d, S, _p(np.ascontiguousarray(Q, np.float32)),
+                                            _p(np.ascontiguousarray(K, np.float32)), _p(out), nthreads))
+    return out
+
+
 # ---------------------------------------------------------------- selection
 def top_p_row(scores, P: float):
     s = np.ascontiguousarray(scores, np.float64)

@@ -513,3 +513,96 @@ def test_gqa_generator_reduces_to_reference():
     ref = O.gen_workload(O.WL_PLANTED, 256, 2, 16, 64, 21)
     for x, y in zip(full, ref):
         assert (x == y).all()
+
+
+# ------------------------------------------------------------------ competitor proxies (test_baselines.cpp)
+def _rand(H, L, d, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((H, L, d)).astype(np.float32), rng.standard_normal((H, L, d)).astype(np.float32))
+
+
+def _literal_antidiagonal(Qh, Kh, S, stride):  # oracles.hpp:115-140, literal enumeration
+    L, d = Qh.shape
+    N = L // S
+    score = np.zeros((N, N))
+    for i in range(N):
+        for q in range(S):
+            t = i * S + q
+            keys = [j * S + (S - 1 - q + r) % S for j in range(i + 1) for r in range(0, S, stride)]
+            keys = [k for k in keys if k <= t]
+            if not keys:
+                continue
+            lg = np.array([np.dot(Qh[t].astype(np.float64), Kh[k].astype(np.float64)) for k in keys]) / np.sqrt(d)
+            p = np.exp(lg - lg.max())
+            p /= p.sum()
+            for k, pk in zip(keys, p):
+                score[i, k // S] += pk
+    return score
+
+
+def test_antidiagonal_stride1_is_exact_mass():  # test_baselines.cpp:40-48
+    Q, K = _rand(2, 128, 8, 3)
+    probe = O.antidiagonal_block_scores(Q, K, 32, 1)
+    mass = O.exact_block_mass(Q, K, 32)
+    tri = np.tril(np.ones((4, 4), bool))
+    assert np.allclose(probe[:, tri], mass[:, tri], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("stride", [2, 4, 8, 16, 32])
+def test_antidiagonal_matches_literal_enumeration(stride):  # test_baselines.cpp:50-61
+    Q, K = _rand(2, 128, 8, 5)
+    probe = O.antidiagonal_block_scores(Q, K, 32, stride)
+    tri = np.tril(np.ones((4, 4), bool))
+    for h in range(2):
+        ref = _literal_antidiagonal(Q[h], K[h], 32, stride)
+        assert np.allclose(probe[h][tri], ref[tri], rtol=1e-9, atol=1e-15)
+
+
+def test_antidiagonal_masks_and_row_mass():  # test_baselines.cpp:63-83
+    Q, K = _rand(1, 128, 8, 9)
+    S, stride = 32, 8
+    probe = O.antidiagonal_block_scores(Q, K, S, stride)
+    for i in range(4):
+        for j in range(i + 1, 4):
+            assert probe[0, i, j] == O.K_MASKED_SCORE
+        rows = sum(1 for q in range(S) if (S - 1 - q) % stride <= i * S + q)
+        assert probe[0, i, : i + 1].sum() == pytest.approx(rows, rel=1e-9)
+
+
+def test_antidiagonal_S1_equals_identity_pre_softmax():  # test_baselines.cpp:85-98
+    Q, K = _rand(1, 32, 8, 11)
+    probe = O.antidiagonal_block_scores(Q, K, 1, 1)
+    c = O.cfg(1, 32, 8, 1, c_q=1, c_k=1, causal_mode=O.PRE_SOFTMAX)
+    Qc, Kc = O.compress(c, Q, K)
+    s = O.proxy_scores(c, Qc, Kc)
+    tri = np.tril(np.ones((32, 32), bool))
+    assert np.allclose(probe[0][tri], s[0][tri], rtol=1e-9, atol=1e-15)
+
+
+def test_antidiagonal_validates_stride():  # test_baselines.cpp:185-189
+    Q, K = _rand(1, 64, 8, 21)
+    for bad in (0, 3):
+        with pytest.raises(O.OracleError, match="stride must divide S"):
+            O.antidiagonal_block_scores(Q, K, 32, bad)
+
+
+def test_last_block_probe_replicates_columns():  # test_baselines.cpp:100-114
+    Q, K = _rand(2, 128, 8, 13)
+    probe = O.last_block_probe_scores(Q, K, 32)
+    for h in range(2):
+        for i in range(4):
+            for j in range(4):
+                assert probe[h, i, j] == (O.K_MASKED_SCORE if j > i else probe[h, 3, j])
+
+
+def test_last_block_probe_single_block_and_uniform_keys():  # test_baselines.cpp:116-136
+    Q, K = _rand(1, 32, 8, 15)
+    probe = O.last_block_probe_scores(Q, K, 32)
+    assert probe[0, 0, 0] == pytest.approx(32.0, rel=1e-9)
+    assert probe[0, 0, 0] == pytest.approx(O.exact_block_mass(Q, K, 32)[0, 0, 0], rel=1e-9)
+    Q, K = _rand(1, 128, 8, 17)
+    K[:] = 0.0
+    probe = O.last_block_probe_scores(Q, K, 32)
+    expect = sum(32.0 / (97.0 + r) for r in range(32))
+    for j in range(3):
+        assert probe[0, 3, j] == pytest.approx(expect, rel=1e-9)
