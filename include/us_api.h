@@ -126,6 +126,16 @@ us_status us_compress(const us_params* p, const void* Q, const void* K, float* Q
 us_status us_select(const us_params* p, const void* Q, const void* K, const us_selection* out,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* select_blocks(proxy, in, cfg, stride) (pipeline.cpp:5-17) for any proxy tag:
+ * US_PROXY_UNISPARSE = us_select; US_PROXY_ANTIDIAGONAL = the XAttention-style
+ * strided anti-diagonal scorer (antidiagonal_block_scores, baselines.cpp:10-52),
+ * per original head (planes = H, no head compression); US_PROXY_LAST_BLOCK is
+ * not implemented on the GPU path (US_ERR_UNSUPPORTED). The workspace must hold
+ * us_proxy_workspace_bytes(p, proxy, stride) bytes. */
+us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, const void* Q, const void* K,
+                          const us_selection* out, void* workspace, size_t workspace_bytes, void* stream);
+size_t us_proxy_workspace_bytes(const us_params* p, int32_t proxy, int32_t stride);
+
 /* build_block_mask (selection.cpp:60-88) on given f32 block scores
  * [B][planes][N][N] (only j <= i read). */
 us_status us_build_block_mask(const us_params* p, const float* scores, const us_selection* out,

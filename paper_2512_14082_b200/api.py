@@ -103,6 +103,10 @@ def lib() -> C.CDLL:
             L.us_compress.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.c_size_t, vp]
             L.us_select.argtypes = [C.POINTER(UsParams), vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
             L.us_build_block_mask.argtypes = [C.POINTER(UsParams), vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
+            L.us_select_proxy.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp, vp, C.POINTER(UsSelection),
+                                          vp, C.c_size_t, vp]
+            L.us_proxy_workspace_bytes.restype = C.c_size_t
+            L.us_proxy_workspace_bytes.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32]
             L.us_sparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_size_t, vp]
             L.us_unisparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
             L.us_dense_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
@@ -284,15 +288,27 @@ def compress(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 
 
 def select_blocks(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64,
                   with_scores: bool = False, with_indices: bool = False,
-                  sync_check: bool = True) -> SparsityReport:
-    """select_blocks(UniSparse, ...) (pipeline.cpp:5-17)."""
+                  sync_check: bool = True, proxy: int = PROXY_UNISPARSE, stride: int = 8) -> SparsityReport:
+    """select_blocks(proxy, in, cfg, stride) (pipeline.cpp:5-17). proxy = PROXY_UNISPARSE
+    (the compressed proxy) or PROXY_ANTIDIAGONAL (XAttention-style, baselines.cpp:10-52;
+    per original head, c_h forced to 1 as in pipeline.cpp:11)."""
     _check_inputs(Q, K)
+    if proxy != PROXY_UNISPARSE:
+        cfg = dataclasses.replace(cfg, c_h=1)
     p = make_params(Q, K, cfg, S, sync_check)
+    need = lib().us_proxy_workspace_bytes(C.byref(p), proxy, stride)
     ws = workspace(p)
+    if ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=Q.device)
+        _ws_cache[torch.cuda.current_device()] = ws
     sel = _alloc_selection(p, with_scores, with_indices)
     ss = _sel_struct(sel)
-    _raise(lib().us_select(C.byref(p), _ptr(Q), _ptr(K), C.byref(ss), _ptr(ws), ws.numel(), _stream()))
-    return make_report(p, sel)
+    _raise(lib().us_select_proxy(C.byref(p), proxy, stride, _ptr(Q), _ptr(K), C.byref(ss), _ptr(ws), ws.numel(),
+                                 _stream()))
+    rep = make_report(p, sel)
+    rep.flops = selection_flops(p, proxy, stride)
+    rep.flops["sparse_attention"] = int(sum(rep.selected)) * 4 * p.S * p.S * p.d_k
+    return rep
 
 
 def build_block_mask(scores: torch.Tensor, cfg: CompressionConfig, H: Optional[int] = None,

@@ -266,7 +266,88 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   pa.lse2 = at<float>(ws, w.lse2);
   pa.scores = at<float>(ws, w.scores);
   pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  pa.x3 = 1;
   return launch_proxy(pa, tKh, tKl, st);
+}
+
+// params whose workspace layout fits the antidiagonal proxy: composite rows of one
+// phase class are L / stride long, like a compression factor of `stride`
+us_params antidiag_params(const us_params& p, int stride) {
+  us_params q = p;
+  q.c_q = q.c_k = stride;
+  q.c_h = 1;
+  q.causal_mode = US_PRE_SOFTMAX_COMPRESSED_CAUSAL;
+  return q;
+}
+
+// antidiagonal_block_scores (baselines.cpp:10-52) into ws.scores [B][H][N][N]: one
+// pass of the proxy kernel per query phase class a (queries t = stride*t' + a sample
+// the keys s = stride*s' + res, res = stride - 1 - a, s <= t), bf16 single-MMA logits
+// (exact products), softmax over the sampled causal keys, region sums accumulated
+// over the classes in a fixed order.
+us_status run_antidiagonal(const us_params& p, int stride, const void* Q, const void* K, void* ws,
+                           cudaStream_t st) {
+  const us_params q = antidiag_params(p, stride);
+  Geo g(q);
+  Ws w = layout(q);
+  const int Lc = g.L / stride;
+  CUtensorMap tK;
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return US_ERR_CUDA;
+  }
+  {
+    // K as (d, stride, B*H_kv*L/stride): box (64, 1, 128) = 128 keys of one phase class
+    cuuint64_t dims[3] = {cuuint64_t(g.D), cuuint64_t(stride), cuuint64_t(g.B) * g.H_kv * Lc};
+    cuuint64_t strides[2] = {cuuint64_t(g.D) * 2, cuuint64_t(g.D) * 2 * stride};
+    cuuint32_t box[3] = {64, 1, 128};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&tK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(K), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (3-D K) failed (" + std::to_string(int(r)) + ")");
+      return US_ERR_CUDA;
+    }
+  }
+  ProxyArgs pa{};
+  pa.B = g.B;
+  pa.Hc = g.H;
+  pa.Lq = Lc;
+  pa.Lk = Lc;
+  pa.N = g.N;
+  pa.D = g.D;
+  pa.rq = g.S / stride;
+  pa.rk = g.S / stride;
+  pa.c_q = stride;
+  pa.c_k = stride;
+  pa.causal_mode = US_PRE_SOFTMAX_COMPRESSED_CAUSAL;
+  pa.kv_planes = g.H_kv;
+  pa.kv_mul = 1;
+  pa.kv_div = g.G;
+  pa.T = (Lc + 127) / 128;
+  pa.sw = proxy_slot_width(pa.rk);
+  pa.part = at<float>(ws, w.part);
+  pa.tmax = at<float>(ws, w.tmax);
+  pa.lse2 = at<float>(ws, w.lse2);
+  pa.scores = at<float>(ws, w.scores);
+  pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  pa.x3 = 0;
+  pa.qraw = static_cast<const uint16_t*>(Q);
+  pa.L = g.L;
+  pa.q_row0 = 0;
+  pa.q_stride = stride;
+  for (int cls = 0; cls < stride; ++cls) {
+    const int res = stride - 1 - cls;
+    pa.q_phase = cls;
+    pa.k_phase = res;
+    pa.live_bias = cls >= res ? 1 : 0;
+    pa.accumulate = cls > 0;
+    us_status s = launch_proxy(pa, tK, tK, st);
+    if (s != US_OK) return s;
+  }
+  return US_OK;
 }
 
 us_status run_select_rows(const us_params& p, const float* scores, int planes, uint32_t* mask,
@@ -461,6 +542,46 @@ us_status us_select(const us_params* p, const void* Q, const void* K, const us_s
   if ((s = run_select_rows(*p, at<float>(workspace, w.scores), g.Hc, mask, out, workspace, st)) != US_OK)
     return s;
   if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "select_blocks");
+  return US_OK;
+}
+
+size_t us_proxy_workspace_bytes(const us_params* p, int32_t proxy, int32_t stride) {
+  if (!p || !check(*p, false).errors.empty()) return 0;
+  if (proxy == US_PROXY_ANTIDIAGONAL && stride > 0) return layout(antidiag_params(*p, stride)).total;
+  return layout(*p).total;
+}
+
+us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, const void* Q, const void* K,
+                          const us_selection* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (proxy == US_PROXY_UNISPARSE) return us_select(p, Q, K, out, workspace, workspace_bytes, stream);
+  us_status s = gate(p, "select_blocks", false);
+  if (s != US_OK) return s;
+  if (proxy != US_PROXY_ANTIDIAGONAL) {
+    set_error("select_blocks: the last-block probe proxy is not implemented on the GPU path");
+    return US_ERR_UNSUPPORTED;
+  }
+  if (stride <= 0 || p->S % stride != 0) {
+    set_error("antidiagonal_block_scores: stride must divide S");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if (!is_pow2(p->S / stride) || p->S / stride > 64) {
+    set_error("select_blocks: S/stride must be a power of two on the GPU path");
+    return US_ERR_UNSUPPORTED;
+  }
+  const us_params q = antidiag_params(*p, stride);
+  if ((s = need_ws(q, workspace, workspace_bytes, "select_blocks")) != US_OK) return s;
+  Geo g(q);
+  Ws w = layout(q);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
+  if ((s = run_antidiagonal(*p, stride, Q, K, workspace, st)) != US_OK) return s;
+  if (out && out->scores)
+    US_CUDA_TRY(cudaMemcpyAsync(out->scores, at<float>(workspace, w.scores), size_t(4) * g.B * g.H * g.N * g.N,
+                                cudaMemcpyDeviceToDevice, st),
+                "scores copy");
+  uint32_t* mask = (out && out->mask_bits) ? out->mask_bits : at<uint32_t>(workspace, w.mask);
+  if ((s = run_select_rows(q, at<float>(workspace, w.scores), g.H, mask, out, workspace, st)) != US_OK) return s;
+  if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(q, workspace, st, "select_blocks");
   return US_OK;
 }
 

@@ -64,6 +64,14 @@ struct ProxyArgs {
   float* lse2;         // [B*Hc][Lq] row log-sum-exp in log2 units
   float* scores;       // [B*Hc][N][N] block scores (j <= i)
   float scale_log2;    // log2(e) / sqrt(d_k)
+  // competitor proxies (x3 = 0): raw bf16 rows of one phase class, single MMA
+  int x3;              // 1: UniSparse fp16x3 on compressed rows; 0: bf16 raw rows
+  const uint16_t* qraw;  // bf16 Q [B][Hc][L][D]
+  int L;               // original sequence length (raw Q row stride per head)
+  int q_row0, q_stride, q_phase;  // query composite row r -> raw row q_row0 + r*q_stride + q_phase
+  int k_phase;         // key phase class (3-D K map: (d, stride, rows/stride))
+  int live_bias;       // live keys of composite row r = r + live_bias
+  int accumulate;      // finalize adds into scores instead of overwriting
 };
 int proxy_slot_width(int rk);
 // One pass (logits, row LSE, slot partials) then the finalize (block scores).

@@ -61,7 +61,7 @@ __device__ __forceinline__ int live_keys(int t, int c_q, int c_k, int Lk, int mo
   return live < Lk ? int(live) : Lk;
 }
 
-template <int D, int SW>
+template <int D, int SW, bool X3>
 __global__ void __launch_bounds__(320, 1)
     proxy_kernel(const __grid_constant__ CUtensorMap tmKh, const __grid_constant__ CUtensorMap tmKl,
                  const ProxyArgs a) {
@@ -82,11 +82,13 @@ __global__ void __launch_bounds__(320, 1)
   const int kplane = b * a.kv_planes + (hc * a.kv_mul) / a.kv_div;
 
   const int r_last = min(r0 + kRows, a.Lq) - 1;
-  const int nkeys = live_keys(r_last, a.c_q, a.c_k, a.Lk, a.causal_mode);
+  // X3: UniSparse composite rows (live rule of the causal mode); !X3: strided raw rows
+  // of a competitor proxy, live keys = row + live_bias (causal by original position)
+  const int nkeys = X3 ? live_keys(r_last, a.c_q, a.c_k, a.Lk, a.causal_mode) : min(a.Lk, r_last + a.live_bias);
   const int n_tiles = (nkeys + kKeys - 1) / kKeys;
   const int i_max = r_last / a.rq;
   const int causal_keys = min(a.Lk, (i_max + 1) * a.rk);
-  const int n_part_tiles = min(n_tiles, (causal_keys + kKeys - 1) / kKeys);
+  const int n_part_tiles = X3 ? min(n_tiles, (causal_keys + kKeys - 1) / kKeys) : n_tiles;
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 8);
@@ -117,18 +119,25 @@ __global__ void __launch_bounds__(320, 1)
         if (t >= kST) mbar_wait(&bar_kempty[s], ((t / kST) + 1) & 1);
         uint8_t* kh = smem + s * 2 * L::kKBytes;
         uint8_t* kl = kh + L::kKBytes;
-        mbar_arrive_expect_tx(&bar_kfull[s], 2 * L::kKBytes);
         const int krow = kplane * a.Lk + t * kKeys;
-        for (int kc = 0; kc < L::kChunks; ++kc) {
-          tma_load_2d_hint(kh + kc * kKeys * 128, &tmKh, &bar_kfull[s], kc * 64, krow, pol);
-          tma_load_2d_hint(kl + kc * kKeys * 128, &tmKl, &bar_kfull[s], kc * 64, krow, pol);
+        if (X3) {
+          mbar_arrive_expect_tx(&bar_kfull[s], 2 * L::kKBytes);
+          for (int kc = 0; kc < L::kChunks; ++kc) {
+            tma_load_2d_hint(kh + kc * kKeys * 128, &tmKh, &bar_kfull[s], kc * 64, krow, pol);
+            tma_load_2d_hint(kl + kc * kKeys * 128, &tmKl, &bar_kfull[s], kc * 64, krow, pol);
+          }
+        } else {
+          // raw bf16 K rows of one phase class: 3-D map (d, stride, rows / stride)
+          mbar_arrive_expect_tx(&bar_kfull[s], L::kKBytes);
+          for (int kc = 0; kc < L::kChunks; ++kc)
+            tma_load_3d_hint(kh + kc * kKeys * 128, &tmKh, &bar_kfull[s], kc * 64, a.k_phase, krow, pol);
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = idesc_f16(kRows, kKeys, /*f16*/ 0, false, false);
+    constexpr uint32_t idesc = idesc_f16(kRows, kKeys, /*f16 or bf16*/ X3 ? 0 : 1, false, false);
     mbar_wait(&bar_q, 0);
     tc_fence_after();
     for (int t = 0; t < n_tiles; ++t) {
@@ -146,9 +155,14 @@ __global__ void __launch_bounds__(320, 1)
             const uint32_t ko = kc * kKeys * 128 + ks * 32;
             const uint32_t qcol = (kc * 4 + ks) * 8;
             const uint64_t bkh = sdesc_sw128(kh + ko, 16, 1024), bkl = sdesc_sw128(kl + ko, 16, 1024);
-            umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkl, idesc, (kc | ks) != 0);
-            umma_f16_ts(d_tmem, tmem + kTQl + qcol, bkh, idesc, 1);
-            umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkh, idesc, 1);
+            if (X3) {
+              umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkl, idesc, (kc | ks) != 0);
+              umma_f16_ts(d_tmem, tmem + kTQl + qcol, bkh, idesc, 1);
+              umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkh, idesc, 1);
+            } else {
+              // bf16 inputs: products are exact in fp32, one MMA per K step
+              umma_f16_ts(d_tmem, tmem + kTQh + qcol, bkh, idesc, (kc | ks) != 0);
+            }
           }
         }
         umma_commit(&bar_kempty[s]);
@@ -166,10 +180,15 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_addr = tmem + (uint32_t(q * 32) << 16);
     {
       // Q hi (group 0) / Q lo (group 1) row -> TMEM, the A operand of every MMA
-      const __half* src = (grp == 0 ? a.qh : a.ql) + ((long long)plane * a.Lq + t_row) * D;
+      // (!X3: group 0 stores the raw bf16 query row t = q_row0 + row * q_stride + q_phase)
+      const uint16_t* src = X3 ? reinterpret_cast<const uint16_t*>((grp == 0 ? a.qh : a.ql) +
+                                                                 ((long long)plane * a.Lq + t_row) * D)
+                               : a.qraw + ((long long)plane * a.L + a.q_row0 + (long long)t_row * a.q_stride +
+                                           a.q_phase) * D;
       const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
       for (int c0 = 0; c0 < D / 2; c0 += 16) {
+        if (!X3 && grp == 1) break;
         uint32_t w16[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -186,8 +205,10 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_q);
     }
-    const int live = row_ok ? live_keys(t_row, a.c_q, a.c_k, a.Lk, a.causal_mode) : 0;
-    const float k2 = ldexpf(a.scale_log2, -(a.exp_q[plane] + a.exp_k[kplane]));
+    const int live = !row_ok ? 0
+                     : X3    ? live_keys(t_row, a.c_q, a.c_k, a.Lk, a.causal_mode)
+                             : max(0, min(a.Lk, t_row + a.live_bias));
+    const float k2 = X3 ? ldexpf(a.scale_log2, -(a.exp_q[plane] + a.exp_k[kplane])) : a.scale_log2;
     float m = -INFINITY, l = 0.f;
     for (int t = grp; t < n_tiles; t += 2) {
       mbar_wait(&bar_sfull[grp], (t >> 1) & 1);
@@ -306,24 +327,25 @@ __global__ void __launch_bounds__(256) proxy_finalize_kernel(const ProxyArgs a) 
         for (int u = 0; u < SPB; ++u) v += __ldg(a.part + (base + r) * NS + s0 + u);
         ps[r] = v;
       }
+      // (a row with no live key — a competitor proxy's first phase-class row — adds 0)
 #pragma unroll
-      for (int r = 0; r < RQ; ++r) acc += ps[r] * ex2_approx(pm[r] - lse_sh[r]);
+      for (int r = 0; r < RQ; ++r) acc += lse_sh[r] == -INFINITY ? 0.f : ps[r] * ex2_approx(pm[r] - lse_sh[r]);
     } else {
       for (int r = 0; r < rq; ++r) {
         const float* pr = a.part + (base + r) * NS + s0;
         float v = 0.f;
         for (int u = 0; u < spb; ++u) v += pr[u];
-        acc += v * ex2_approx(a.tmax[base + r] - lse_sh[r]);
+        acc += lse_sh[r] == -INFINITY ? 0.f : v * ex2_approx(a.tmax[base + r] - lse_sh[r]);
       }
     }
-    out[j] = acc;
+    out[j] = a.accumulate ? out[j] + acc : acc;
   }
 }
 
-template <int D, int SW>
-us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
+template <int D, int SW, bool X3>
+us_status launch_proxy_x(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
   const int smem = ProxySmem<D>::kBytes + 1024;
-  auto kern = proxy_kernel<D, SW>;
+  auto kern = proxy_kernel<D, SW, X3>;
   static bool attr_set = false;  // benign race: idempotent attribute set
   if (!attr_set) {
     US_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
@@ -338,6 +360,11 @@ us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmKh, const CUte
   else proxy_finalize_kernel<SW, 0, 0><<<fgrid, 256, 0, st>>>(a);
   US_LAUNCH_CHECK("proxy_finalize_kernel");
   return US_OK;
+}
+
+template <int D, int SW>
+us_status launch_proxy_t(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
+  return a.x3 ? launch_proxy_x<D, SW, true>(a, tmKh, tmKl, st) : launch_proxy_x<D, SW, false>(a, tmKh, tmKl, st);
 }
 
 template <int D>

@@ -271,3 +271,28 @@ def test_attention_impls_agree(H, H_kv, d):
                 assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
     finally:
         lib.us_set_attention_impl(1)
+
+
+# ------------------------------------------------------------------ competitor proxy (antidiagonal)
+@pytest.mark.parametrize("H,H_kv,d,stride,P", [(4, 2, 128, 8, 0.9), (2, 2, 64, 4, 0.95), (4, 1, 128, 16, 0.9)])
+def test_antidiagonal_proxy_matches_reference(H, H_kv, d, stride, P):
+    """XAttention-style strided anti-diagonal scorer (baselines.cpp:10-52) on the GPU:
+    scores within fp32-class error of the fp64 restatement, masks equal the
+    reference rule on the reference scores."""
+    L, S = 2048, 64
+    Q, K, V, _ = O.gen_workload(O.WL_PLANTED, L, H, d, S, 77 + stride, H_kv=H_kv, gain=8.0)
+    Q, K = O.bf16_round(Q), O.bf16_round(K)
+    cfg = us().CompressionConfig(P=P)
+    rep = us().select_blocks(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), cfg, proxy=us().api.PROXY_ANTIDIAGONAL,
+                             stride=stride, with_scores=True)
+    torch.cuda.synchronize()
+    N = L // S
+    tri = np.tril(np.ones((N, N), bool))
+    gs = rep.mask.scores[0].cpu().numpy()
+    rs = O.antidiagonal_block_scores(Q, K, S, stride)
+    big = rs[:, tri] > 1e-6
+    rel = np.abs(gs[:, tri] - rs[:, tri])[big] / rs[:, tri][big]
+    assert np.median(rel) < 1e-5 and rel.max() < 1e-3, (np.median(rel), rel.max())
+    ref_mask, _ = O.build_block_mask(rs, H, 1, P)
+    got = rep.mask.dense_mask()[0].cpu().numpy()
+    assert int((got != ref_mask).sum()) == 0
