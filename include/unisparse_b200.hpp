@@ -279,6 +279,31 @@ inline CompressedViews compress(const AttentionInputs& in, const CompressionConf
   return v;
 }
 
+enum class ProxyTag { UniSparse = US_PROXY_UNISPARSE, Antidiagonal = US_PROXY_ANTIDIAGONAL,
+                      LastBlockProbe = US_PROXY_LAST_BLOCK };
+
+// select_blocks(proxy, in, cfg, stride) (pipeline.hpp:19-20): the competitor proxies
+// score per original head (c_h forced to 1, pipeline.cpp:11).
+inline SparsityReport select_blocks(ProxyTag proxy, const AttentionInputs& in, const CompressionConfig& cfg,
+                                    int stride = 8) {
+  CompressionConfig c = cfg;
+  if (proxy != ProxyTag::UniSparse) c.c_h = 1;
+  const us_params p = detail::params(in, c, true);
+  detail::validate("select_blocks", p, proxy == ProxyTag::UniSparse);
+  BlockMask m = detail::alloc_mask(p);
+  DeviceBuffer<uint8_t> ws(us_proxy_workspace_bytes(&p, int32_t(proxy), stride) + 256);
+  us_selection sel{m.bits.data(), m.counts.data(), m.coverage.data(), nullptr, nullptr};
+  detail::raise(us_select_proxy(&p, int32_t(proxy), stride, in.Q, in.K, &sel, ws.data(), ws.size(), in.stream));
+  SparsityReport r = detail::report(p, std::move(m));
+  uint64_t f[6];
+  detail::raise(us_selection_flops(&p, int32_t(proxy), stride, f));
+  r.flops.compression = f[0];
+  r.flops.compressed_qk = f[1];
+  r.flops.softmax_aggregation = f[2];
+  r.flops.top_p = f[3];
+  return r;
+}
+
 inline SparsityReport select_blocks(const AttentionInputs& in, const CompressionConfig& cfg) {
   const us_params p = detail::params(in, cfg, true);
   detail::validate("select_blocks", p);

@@ -129,8 +129,9 @@ us_status us_select(const us_params* p, const void* Q, const void* K, const us_s
 /* select_blocks(proxy, in, cfg, stride) (pipeline.cpp:5-17) for any proxy tag:
  * US_PROXY_UNISPARSE = us_select; US_PROXY_ANTIDIAGONAL = the XAttention-style
  * strided anti-diagonal scorer (antidiagonal_block_scores, baselines.cpp:10-52),
- * per original head (planes = H, no head compression); US_PROXY_LAST_BLOCK is
- * not implemented on the GPU path (US_ERR_UNSUPPORTED). The workspace must hold
+ * US_PROXY_LAST_BLOCK = the FlexPrefill-style last-block probe
+ * (last_block_probe_scores, baselines.cpp:54-87); both per original head
+ * (planes = H, no head compression, pipeline.cpp:11). The workspace must hold
  * us_proxy_workspace_bytes(p, proxy, stride) bytes. */
 us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, const void* Q, const void* K,
                           const us_selection* out, void* workspace, size_t workspace_bytes, void* stream);

@@ -548,6 +548,7 @@ us_status us_select(const us_params* p, const void* Q, const void* K, const us_s
 size_t us_proxy_workspace_bytes(const us_params* p, int32_t proxy, int32_t stride) {
   if (!p || !check(*p, false).errors.empty()) return 0;
   if (proxy == US_PROXY_ANTIDIAGONAL && stride > 0) return layout(antidiag_params(*p, stride)).total;
+  if (proxy == US_PROXY_LAST_BLOCK) return layout(antidiag_params(*p, p->S)).total;
   return layout(*p).total;
 }
 
@@ -556,9 +557,45 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
   if (proxy == US_PROXY_UNISPARSE) return us_select(p, Q, K, out, workspace, workspace_bytes, stream);
   us_status s = gate(p, "select_blocks", false);
   if (s != US_OK) return s;
+  if (proxy == US_PROXY_LAST_BLOCK) {
+    // last_block_probe_scores (baselines.cpp:54-87), planes = H. Workspace: the
+    // layout of one composite row per block (c = S); the chunk statistics, row LSE
+    // and column masses live in its (large) slot-partial region.
+    const us_params q = antidiag_params(*p, p->S);
+    if ((s = need_ws(q, workspace, workspace_bytes, "select_blocks")) != US_OK) return s;
+    Geo g(q);
+    Ws w = layout(q);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
+    LastBlockArgs la{};
+    la.B = g.B;
+    la.H = g.H;
+    la.H_kv = g.H_kv;
+    la.L = g.L;
+    la.N = g.N;
+    la.D = g.D;
+    la.Q = static_cast<const uint16_t*>(Q);
+    la.K = static_cast<const uint16_t*>(K);
+    la.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+    const size_t stat = size_t(g.B) * g.H * (g.L / 256) * 64;
+    la.cmax = at<float>(workspace, w.part);
+    la.csum = la.cmax + stat;
+    la.lse2 = la.csum + stat;
+    la.colmass = la.lse2 + size_t(g.B) * g.H * 64;
+    la.scores = at<float>(workspace, w.scores);
+    if ((s = launch_last_block_probe(la, st)) != US_OK) return s;
+    if (out && out->scores)
+      US_CUDA_TRY(cudaMemcpyAsync(out->scores, la.scores, size_t(4) * g.B * g.H * g.N * g.N,
+                                  cudaMemcpyDeviceToDevice, st),
+                  "scores copy");
+    uint32_t* mask = (out && out->mask_bits) ? out->mask_bits : at<uint32_t>(workspace, w.mask);
+    if ((s = run_select_rows(q, la.scores, g.H, mask, out, workspace, st)) != US_OK) return s;
+    if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(q, workspace, st, "select_blocks");
+    return US_OK;
+  }
   if (proxy != US_PROXY_ANTIDIAGONAL) {
-    set_error("select_blocks: the last-block probe proxy is not implemented on the GPU path");
-    return US_ERR_UNSUPPORTED;
+    set_error("select_blocks: unknown proxy");
+    return US_ERR_INVALID_ARGUMENT;
   }
   if (stride <= 0 || p->S % stride != 0) {
     set_error("antidiagonal_block_scores: stride must divide S");

@@ -78,6 +78,20 @@ int proxy_slot_width(int rk);
 us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl,
                        cudaStream_t st);
 
+// ---------------------------------------------------------------- last-block probe (competitor)
+struct LastBlockArgs {
+  int B, H, H_kv, L, N, D;
+  const uint16_t* Q;   // bf16 [B][H][L][D]
+  const uint16_t* K;   // bf16 [B][H_kv][L][D]
+  float scale_log2;
+  float* cmax;         // [B*H][L/256][64] chunk maxima (log2 units)
+  float* csum;         // [B*H][L/256][64] chunk sums
+  float* lse2;         // [B*H][64]
+  float* colmass;      // [B*H][N]
+  float* scores;       // [B*H][N][N] (j <= i)
+};
+us_status launch_last_block_probe(const LastBlockArgs& a, cudaStream_t st);
+
 // ---------------------------------------------------------------- selection (a4-a5)
 struct SelectArgs {
   const float* scores;  // [rows][N] (row = (b*planes + p)*N + i), j <= i read

@@ -185,6 +185,12 @@ static void gpu_tests() {
   }
   const double cosv = dot / std::sqrt(na * nb);
   CHECK(cosv > 0.9);
+  // competitor proxies through the same selection machinery (test_baselines.cpp:157-183)
+  for (u::ProxyTag tag : {u::ProxyTag::Antidiagonal, u::ProxyTag::LastBlockProbe}) {
+    u::SparsityReport rp = u::select_blocks(tag, in, cfg, 8);
+    CHECK(rp.mask.H == H && rp.mask.c_h == 1);
+    CHECK(rp.mask.selected_total() >= int64_t(H) * N);  // every causal row keeps >= 1 block
+  }
   std::printf("gpu: rho=%.4f selected=%lld cos(sparse,dense)=%.5f %s\n", r.report.rho_mean, (long long)sel,
               cosv, g_fail ? "FAILED" : "ok");
 }

@@ -296,3 +296,24 @@ def test_antidiagonal_proxy_matches_reference(H, H_kv, d, stride, P):
     ref_mask, _ = O.build_block_mask(rs, H, 1, P)
     got = rep.mask.dense_mask()[0].cpu().numpy()
     assert int((got != ref_mask).sum()) == 0
+
+
+@pytest.mark.parametrize("H,H_kv,d,P", [(4, 2, 128, 0.9), (2, 2, 64, 0.95)])
+def test_last_block_probe_matches_reference(H, H_kv, d, P):
+    """FlexPrefill-style last-block probe (baselines.cpp:54-87) on the GPU: column
+    masses within fp32-class error, masks equal the reference rule."""
+    L, S = 2048, 64
+    Q, K, V, _ = O.gen_workload(O.WL_PLANTED, L, H, d, S, 91, H_kv=H_kv, gain=8.0)
+    Q, K = O.bf16_round(Q), O.bf16_round(K)
+    rep = us().select_blocks(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), us().CompressionConfig(P=P),
+                             proxy=us().api.PROXY_LAST_BLOCK, with_scores=True)
+    torch.cuda.synchronize()
+    N = L // S
+    tri = np.tril(np.ones((N, N), bool))
+    gs = rep.mask.scores[0].cpu().numpy()
+    rs = O.last_block_probe_scores(Q, K, S)
+    big = rs[:, tri] > 1e-6
+    rel = np.abs(gs[:, tri] - rs[:, tri])[big] / rs[:, tri][big]
+    assert np.median(rel) < 1e-5 and rel.max() < 1e-3, (np.median(rel), rel.max())
+    ref_mask, _ = O.build_block_mask(rs, H, 1, P)
+    assert int((rep.mask.dense_mask()[0].cpu().numpy() != ref_mask).sum()) == 0

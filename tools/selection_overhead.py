@@ -12,7 +12,8 @@ L = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 H, H_kv, d, gain = 32, 8, 128, 9.0
 Q, K, V = workloads.planted_blocks(L, H, H_kv, d, 64, seed=2512, gain=gain)
 out = {"L": L, "heads": H, "kv_heads": H_kv, "gain": gain}
-for name, proxy, stride in (("unisparse", us.api.PROXY_UNISPARSE, 8), ("antidiagonal_s8", us.api.PROXY_ANTIDIAGONAL, 8)):
+for name, proxy, stride in (("unisparse", us.api.PROXY_UNISPARSE, 8), ("antidiagonal_s8", us.api.PROXY_ANTIDIAGONAL, 8),
+                            ("last_block_probe", us.api.PROXY_LAST_BLOCK, 8)):
     for P in (0.9, 0.95):
         cfg = us.CompressionConfig(P=P)
         run = lambda: us.select_blocks(Q, K, cfg, proxy=proxy, stride=stride, sync_check=False)
