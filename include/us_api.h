@@ -174,6 +174,13 @@ us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, 
  * function; the environment variable US_ATTN_IMPL sets the initial choice. */
 us_status us_set_attention_impl(int32_t impl);
 
+/* Tile pairing inside an attention.cu CTA (calibration knob, process-wide):
+ * 1 = pair the CTA's four query groups into its two M=128 tiles so that the
+ * longer tile's step count is smallest (default), 0 = fixed pairing (01|23).
+ * Outputs are bit-identical either way; the environment variable
+ * US_ATTN_PAIRING sets the initial choice. */
+us_status us_set_attention_pairing(int32_t on);
+
 /* Number of kernel launches the last successful call on this thread issued. */
 int32_t us_last_launch_count(void);
 

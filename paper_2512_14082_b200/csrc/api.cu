@@ -385,6 +385,18 @@ int attention_impl() {
   return v;
 }
 
+// Calibration knob: US_ATTN_PAIRING=0 keeps the fixed (01|23) tile pairing.
+std::atomic<int> g_attn_pairing{-1};
+int attention_pairing() {
+  int v = g_attn_pairing.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = std::getenv("US_ATTN_PAIRING");
+    v = (e && std::atoi(e) == 0) ? 0 : 1;
+    g_attn_pairing.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
                         const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st) {
   Geo g(p);
@@ -402,6 +414,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.W = g.W;
   a.D = g.D;
   a.group_mode = (g.G % 4 == 0) ? 0 : (g.G == 2 ? 1 : 2);
+  a.pairing = attention_pairing();
   a.heads_per_plane = hpp;
   a.planes = g.H / hpp;
   a.mask = mask;
@@ -494,6 +507,15 @@ us_status us_set_attention_impl(int32_t impl) {
     return US_ERR_INVALID_ARGUMENT;
   }
   g_attn_impl.store(impl, std::memory_order_relaxed);
+  return US_OK;
+}
+
+us_status us_set_attention_pairing(int32_t on) {
+  if (on != 0 && on != 1) {
+    set_error("us_set_attention_pairing: on must be 0 or 1");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  g_attn_pairing.store(on, std::memory_order_relaxed);
   return US_OK;
 }
 

@@ -120,6 +120,7 @@ struct AttnArgs {
   __nv_bfloat16* O;     // [B][H][L][D]
   float* lse;           // [B][H][L] (nullable)
   float scale_log2;
+  int pairing;          // 1: pair the CTA's groups into tiles by union size (0: fixed 01|23)
 };
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);

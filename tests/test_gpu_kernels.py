@@ -273,6 +273,36 @@ def test_attention_impls_agree(H, H_kv, d):
         lib.us_set_attention_impl(1)
 
 
+@pytest.mark.parametrize("H,H_kv,density", [(8, 2, 0.3), (16, 4, 0.15), (8, 1, 0.6)])
+def test_attention_tile_pairing_is_invisible(H, H_kv, density):
+    """The per-CTA tile pairing (groups paired by union size) only changes which
+    tile / lanes a query group runs in: outputs and lse are bit-identical to the
+    fixed (01|23) pairing. Per-head densities differ so the pairing does move."""
+    import ctypes
+    rng = np.random.default_rng(H * 10 + H_kv)
+    B, L, d = 1, 2048, 128
+    N = L // 64
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    dens = density * rng.uniform(0.3, 1.7, size=(1, H, 1, 1))
+    mask = rng.random((B, H, N, N)) < dens
+    mask &= np.tril(np.ones((N, N), bool))
+    mask[..., np.arange(N), np.arange(N)] = True
+    bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
+    q, k, v = to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V)
+    lib = us().api.lib()
+    lib.us_set_attention_pairing.argtypes = [ctypes.c_int32]
+    try:
+        out = []
+        for on in (0, 1):
+            assert lib.us_set_attention_pairing(on) == 0
+            Og, lseg = us().block_sparse_attention(q, k, v, bits)
+            out.append((Og.clone(), lseg.clone()))
+        assert torch.equal(out[0][0], out[1][0])
+        assert torch.equal(out[0][1], out[1][1])
+    finally:
+        lib.us_set_attention_pairing(1)
+
+
 # ------------------------------------------------------------------ competitor proxy (antidiagonal)
 @pytest.mark.parametrize("H,H_kv,d,stride,P", [(4, 2, 128, 8, 0.9), (2, 2, 64, 4, 0.95), (4, 1, 128, 16, 0.9)])
 def test_antidiagonal_proxy_matches_reference(H, H_kv, d, stride, P):
