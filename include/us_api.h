@@ -160,6 +160,40 @@ us_status us_dense_attention(const us_params* p, const void* Q, const void* K, c
                              void* O, float* lse, void* workspace, size_t workspace_bytes,
                              void* stream);
 
+/* ---- quality metrics on GPU outputs: the reference's
+ * metrics.cpp:100-224 as used by run_experiment (experiment.cpp:280-437).
+ * Scalar results go to HOST pointers; these calls synchronize the stream. */
+
+/* exact_block_mass (attention.cpp:56-86): for head h and query block i, the mass
+ * of the token-level causal softmax of Q_h K_{h/G}^T / sqrt(d_k) on key block j
+ * (bf16 products, fp32 accumulation), f32 [B][H][N][N]; j > i holds the
+ * reference's kMaskedScore (-FLT_MAX, types.hpp:32). The
+ * workspace must hold us_mass_workspace_bytes(p) bytes (it grows as H * L^2). */
+us_status us_exact_block_mass(const us_params* p, const void* Q, const void* K, float* mass, void* workspace,
+                              size_t workspace_bytes, void* stream);
+size_t us_mass_workspace_bytes(const us_params* p);
+
+/* Workspace of the three metric calls below for these params. */
+size_t us_metrics_workspace_bytes(const us_params* p);
+
+/* output_fidelity (metrics.cpp:118-153) of bf16 O_test against bf16 O_ref, both
+ * [B][H][L][d_k]: out3 = {max_abs, mean_rel, cosine} (fp64, the reference's
+ * per-row sequential sums). */
+us_status us_output_fidelity(const us_params* p, const void* O_test, const void* O_ref, double* out3,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* block_recall (metrics.cpp:155-176): mask planes [B][H/heads_per_plane][N][W]
+ * against reference block scores ref f32 [B][H][N][N]; k in [1, N]. */
+us_status us_block_recall(const us_params* p, const uint32_t* mask_bits, int32_t heads_per_plane, const float* ref,
+                          int32_t k, double* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* mean_row_spearman (metrics.cpp:201-224): proxy scores f32 [B][H/c_h][N][N]
+ * (c_h = p->c_h) against ref f32 [B][H][N][N], rows i >= 1; flat rows count as
+ * undefined. */
+us_status us_mean_row_spearman(const us_params* p, const float* proxy, const float* ref, double* mean,
+                               int64_t* defined, int64_t* undefined, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
 /* Reads and clears the device-side data-error word of a workspace
  * (synchronizes the stream). */
 us_status us_check_device_errors(const us_params* p, void* workspace, void* stream);

@@ -834,6 +834,89 @@ int or_output_fidelity(const float* test, const float* ref, int H, int L, int d,
   return 0;
 }
 
+// argsort_desc / average_ranks (metrics.cpp:17-40): stable orders, average ranks for ties.
+static std::vector<int> argsort_desc_or(const double* v, int n) {
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return v[a] > v[b]; });
+  return order;
+}
+static std::vector<double> average_ranks_or(const double* v, int n) {
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return v[a] < v[b]; });
+  std::vector<double> ranks(n);
+  int i = 0;
+  while (i < n) {
+    int j = i;
+    while (j + 1 < n && v[order[j + 1]] == v[order[i]]) ++j;
+    const double r = 0.5 * (i + j) + 1.0;
+    for (int t = i; t <= j; ++t) ranks[order[t]] = r;
+    i = j + 1;
+  }
+  return ranks;
+}
+
+// spearman_rho (metrics.cpp:100-116); returns 0 and sets *defined = 0 for a flat side.
+int or_spearman_rho(const double* a, const double* b, int n, double* rho, int* defined) {
+  if (n < 2) return fail("spearman_rho: need at least 2 values");
+  const auto ra = average_ranks_or(a, n), rb = average_ranks_or(b, n);
+  const double mean = (double(n) + 1.0) / 2.0;
+  double va = 0.0, vb = 0.0, cov = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double da = ra[i] - mean, db = rb[i] - mean;
+    va += da * da;
+    vb += db * db;
+    cov += da * db;
+  }
+  *defined = !(va == 0.0 || vb == 0.0);
+  *rho = *defined ? cov / std::sqrt(va * vb) : 0.0;
+  return 0;
+}
+
+// block_recall (metrics.cpp:155-176): mask [H][N][N] bytes, reference scores [H][N][N].
+int or_block_recall(const uint8_t* mask, const double* ref, int H, int N, int k, double* out) {
+  if (k < 1 || k > N) return fail("block_recall: k out of range");
+  double sum = 0.0;
+  int64_t rows = 0;
+  for (int h = 0; h < H; ++h)
+    for (int i = 0; i < N; ++i) {
+      const int k_eff = std::min(k, i + 1);
+      const double* row = ref + (size_t(h) * N + i) * N;
+      const auto order = argsort_desc_or(row, i + 1);
+      int hit = 0;
+      for (int t = 0; t < k_eff; ++t) hit += mask[(size_t(h) * N + i) * N + order[t]] ? 1 : 0;
+      sum += double(hit) / double(k_eff);
+      ++rows;
+    }
+  *out = sum / double(rows);
+  return 0;
+}
+
+// mean_row_spearman (metrics.cpp:201-224): proxy [H/c_h][N][N], reference [H][N][N].
+int or_mean_row_spearman(const double* proxy, const double* ref, int H, int N, int c_h, double* mean,
+                         int64_t* defined, int64_t* undefined) {
+  if (c_h <= 0 || H % c_h != 0) return fail("mean_row_spearman: head counts disagree");
+  double sum = 0.0;
+  int64_t d = 0, u = 0;
+  for (int h = 0; h < H; ++h)
+    for (int i = 1; i < N; ++i) {
+      double rho;
+      int def;
+      or_spearman_rho(proxy + (size_t(h / c_h) * N + i) * N, ref + (size_t(h) * N + i) * N, i + 1, &rho, &def);
+      if (def) {
+        sum += rho;
+        ++d;
+      } else {
+        ++u;
+      }
+    }
+  *mean = d ? sum / double(d) : 0.0;
+  *defined = d;
+  *undefined = u;
+  return 0;
+}
+
 // unisparse_attn (pipeline.cpp:19-24): compress -> proxy -> mask -> sparse attention.
 int or_unisparse_attn(const or_cfg* cfg, const float* Q, const float* K, const float* V,
                       float* O, double* lse, uint8_t* mask, double* coverage, int nthreads) {

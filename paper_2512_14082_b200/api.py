@@ -122,6 +122,14 @@ def lib() -> C.CDLL:
             L.us_profile_enable.argtypes = [C.c_int32]
             L.us_profile_read.argtypes = [C.c_void_p, C.c_int32]
             L.us_profile_read.restype = C.c_int32
+            L.us_mass_workspace_bytes.restype = C.c_size_t
+            L.us_mass_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+            L.us_metrics_workspace_bytes.restype = C.c_size_t
+            L.us_metrics_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+            L.us_exact_block_mass.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
+            L.us_output_fidelity.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
+            L.us_block_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
+            L.us_mean_row_spearman.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         return _lib
 
 
@@ -544,3 +552,77 @@ def load_mask_json(path: str):
     _raise(lib().us_load_mask_json(path.encode(), C.byref(H), C.byref(N), C.byref(P), bits.ctypes.data, bits.size))
     m = ((bits[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(H.value, N.value, W * 32)
     return m[..., : N.value], P.value
+
+
+# ------------------------------------------------------------------ quality metrics (§8f-4)
+def _scratch(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def _metric_params(B: int, H: int, L: int, d: int, S: int = 64, c_h: int = 1) -> UsParams:
+    return UsParams(B, H, H, L, d, S, 1, 1, c_h, 0, 0, 0, 1.0, 0, 0, 0)
+
+
+def exact_block_mass(Q: torch.Tensor, K: torch.Tensor, S: int = 64) -> torch.Tensor:
+    """exact_block_mass (attention.cpp:56-86): f32 [B, H, N, N] causal attention mass
+    per (query block, key block), j <= i written (kMaskedScore above the diagonal)."""
+    _check_inputs(Q, K)
+    p = make_params(Q, K, CompressionConfig(c_q=1, c_k=1, c_h=1), S)
+    B, H, L, _ = _bhld(Q)
+    N = L // S
+    mass = torch.full((B, H, N, N), -torch.finfo(torch.float32).max, dtype=torch.float32, device=Q.device)
+    ws = _scratch(lib().us_mass_workspace_bytes(C.byref(p)), Q.device)
+    _raise(lib().us_exact_block_mass(C.byref(p), _ptr(Q), _ptr(K), _ptr(mass), _ptr(ws), ws.numel(), _stream()))
+    return mass
+
+
+def output_fidelity(O_test: torch.Tensor, O_ref: torch.Tensor) -> dict:
+    """output_fidelity (metrics.cpp:118-153) of two bf16 [B, H, L, d] outputs."""
+    if O_test.shape != O_ref.shape:
+        raise ValueError("output_fidelity: shape mismatch")
+    _check_inputs(O_test, O_ref)
+    B, H, L, d = _bhld(O_test)
+    p = _metric_params(B, H, L, d)
+    ws = _scratch(lib().us_metrics_workspace_bytes(C.byref(p)), O_test.device)
+    out = (C.c_double * 3)()
+    _raise(lib().us_output_fidelity(C.byref(p), _ptr(O_test.contiguous()), _ptr(O_ref.contiguous()), out,
+                                    _ptr(ws), ws.numel(), _stream()))
+    return {"max_abs": out[0], "mean_rel": out[1], "cosine": out[2]}
+
+
+def block_recall(mask_bits: torch.Tensor, ref: torch.Tensor, k: int, heads_per_plane: int = 1,
+                 S: int = 64) -> float:
+    """block_recall (metrics.cpp:155-176): mask planes int32 [B, planes, N, W] against
+    reference block scores f32 [B, H, N, N]."""
+    if ref.dim() == 3:
+        ref = ref.unsqueeze(0)
+    B, H, N, _ = ref.shape
+    if mask_bits.dim() == 3:
+        mask_bits = mask_bits.unsqueeze(0)
+    if mask_bits.shape[1] * heads_per_plane != H:
+        raise ValueError("block_recall: reference must hold one plane per mask head")
+    p = _metric_params(B, H, N * S, 64, S)
+    ws = _scratch(lib().us_metrics_workspace_bytes(C.byref(p)), ref.device)
+    out = C.c_double(0.0)
+    _raise(lib().us_block_recall(C.byref(p), _ptr(mask_bits.contiguous()), heads_per_plane,
+                                 _ptr(ref.float().contiguous()), int(k), C.byref(out), _ptr(ws), ws.numel(),
+                                 _stream()))
+    return out.value
+
+
+def mean_row_spearman(proxy: torch.Tensor, ref: torch.Tensor, c_h: int, S: int = 64):
+    """mean_row_spearman (metrics.cpp:201-224) -> (mean, defined, undefined): proxy
+    scores f32 [B, H/c_h, N, N] against ref f32 [B, H, N, N]."""
+    if ref.dim() == 3:
+        ref = ref.unsqueeze(0)
+    if proxy.dim() == 3:
+        proxy = proxy.unsqueeze(0)
+    B, H, N, _ = ref.shape
+    if c_h <= 0 or H % c_h != 0 or proxy.shape[1] != H // c_h or proxy.shape[2] != N:
+        raise ValueError("mean_row_spearman: head counts disagree")
+    p = _metric_params(B, H, N * S, 64, S, c_h)
+    ws = _scratch(lib().us_metrics_workspace_bytes(C.byref(p)), ref.device)
+    mean, d, u = C.c_double(0.0), C.c_int64(0), C.c_int64(0)
+    _raise(lib().us_mean_row_spearman(C.byref(p), _ptr(proxy.float().contiguous()), _ptr(ref.float().contiguous()),
+                                      C.byref(mean), C.byref(d), C.byref(u), _ptr(ws), ws.numel(), _stream()))
+    return mean.value, d.value, u.value

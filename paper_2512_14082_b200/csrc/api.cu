@@ -644,6 +644,130 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
   return US_OK;
 }
 
+// ---------------------------------------------------------------- quality metrics (§8f-4)
+size_t us_mass_workspace_bytes(const us_params* p) {
+  if (!p || !check(*p, false).errors.empty()) return 0;
+  return layout(antidiag_params(*p, 1)).total;
+}
+
+us_status us_exact_block_mass(const us_params* p, const void* Q, const void* K, float* mass, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  // exact_block_mass (attention.cpp:56-86) = the strided scorer at stride 1: every
+  // query row against its causal keys (live = r + 1), bf16 products accumulated in
+  // fp32, row softmax, block sums — the proxy kernel's raw-input mode.
+  us_status s = gate(p, "exact_block_mass", false);
+  if (s != US_OK) return s;
+  if (!mass) {
+    set_error("exact_block_mass: null output");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  const us_params q = antidiag_params(*p, 1);
+  if ((s = need_ws(q, workspace, workspace_bytes, "exact_block_mass")) != US_OK) return s;
+  Geo g(q);
+  Ws w = layout(q);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
+  if ((s = run_antidiagonal(*p, 1, Q, K, workspace, st)) != US_OK) return s;
+  US_CUDA_TRY(cudaMemcpyAsync(mass, at<float>(workspace, w.scores), size_t(4) * g.B * g.H * g.N * g.N,
+                              cudaMemcpyDeviceToDevice, st),
+              "mass copy");
+  return launch_fill_upper(mass, (long long)g.B * g.H, g.N, st);
+}
+
+size_t us_metrics_workspace_bytes(const us_params* p) {
+  if (!p || !check(*p, false).errors.empty()) return 0;
+  const size_t rows_l = size_t(p->B) * p->H * p->L, rows_n = size_t(p->B) * p->H * (p->L / p->S);
+  return 256 + std::max(24 * rows_l, 9 * rows_n + 256);
+}
+
+namespace {
+us_status metrics_ws(const us_params* p, void* ws, size_t bytes, const char* who) {
+  const size_t need = us_metrics_workspace_bytes(p);
+  if (!ws || bytes < need) {
+    set_error(std::string(who) + ": workspace of " + std::to_string(need) + " bytes required");
+    return US_ERR_WORKSPACE;
+  }
+  return US_OK;
+}
+}  // namespace
+
+us_status us_output_fidelity(const us_params* p, const void* O_test, const void* O_ref, double* out3,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  us_status s = gate(p, "output_fidelity", false);
+  if (s != US_OK) return s;
+  if (!O_test || !O_ref || !out3) {
+    set_error("output_fidelity: null argument");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if ((s = metrics_ws(p, workspace, workspace_bytes, "output_fidelity")) != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* res = at<double>(workspace, 0);
+  const long long rows = (long long)p->B * p->H * p->L;
+  if ((s = launch_output_fidelity(rows, p->d_k, static_cast<const uint16_t*>(O_test),
+                                  static_cast<const uint16_t*>(O_ref), at<double>(workspace, 256), res, st)) != US_OK)
+    return s;
+  US_CUDA_TRY(cudaMemcpyAsync(out3, res, 3 * sizeof(double), cudaMemcpyDeviceToHost, st), "fidelity readback");
+  US_CUDA_TRY(cudaStreamSynchronize(st), "output_fidelity");
+  return US_OK;
+}
+
+us_status us_block_recall(const us_params* p, const uint32_t* mask_bits, int32_t heads_per_plane, const float* ref,
+                          int32_t k, double* out, void* workspace, size_t workspace_bytes, void* stream) {
+  us_status s = gate(p, "block_recall", false);
+  if (s != US_OK) return s;
+  const int N = p->L / p->S;
+  if (k < 1 || k > N) {
+    set_error("block_recall: k out of range");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if (heads_per_plane <= 0 || p->H % heads_per_plane != 0 || !mask_bits || !ref || !out) {
+    set_error("block_recall: reference must hold one plane per mask head");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if ((s = metrics_ws(p, workspace, workspace_bytes, "block_recall")) != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* res = at<double>(workspace, 0);
+  if ((s = launch_block_recall(p->B, p->H, N, (N + 31) / 32, p->H / heads_per_plane, heads_per_plane, k, mask_bits,
+                               ref, at<double>(workspace, 256), res, st)) != US_OK)
+    return s;
+  US_CUDA_TRY(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, st), "recall readback");
+  US_CUDA_TRY(cudaStreamSynchronize(st), "block_recall");
+  return US_OK;
+}
+
+us_status us_mean_row_spearman(const us_params* p, const float* proxy, const float* ref, double* mean,
+                               int64_t* defined, int64_t* undefined, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (p && (p->c_h <= 0 || p->H <= 0 || p->H % p->c_h != 0)) {
+    set_error("mean_row_spearman: head counts disagree");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  us_status s = gate(p, "mean_row_spearman", false);
+  if (s != US_OK) return s;
+  if (!proxy || !ref || !mean) {
+    set_error("mean_row_spearman: null argument");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if ((s = metrics_ws(p, workspace, workspace_bytes, "mean_row_spearman")) != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int N = p->L / p->S;
+  const long long rows = (long long)p->B * p->H * N;
+  double* res = at<double>(workspace, 0);
+  long long* ndef = at<long long>(workspace, 64);
+  double* row_val = at<double>(workspace, 256);
+  uint8_t* def = reinterpret_cast<uint8_t*>(row_val + rows);
+  if ((s = launch_row_spearman(p->B, p->H, N, p->c_h, proxy, ref, row_val, def, res, ndef, st)) != US_OK) return s;
+  long long host_def = 0;
+  US_CUDA_TRY(cudaMemcpyAsync(mean, res, sizeof(double), cudaMemcpyDeviceToHost, st), "spearman readback");
+  US_CUDA_TRY(cudaMemcpyAsync(&host_def, ndef, sizeof(long long), cudaMemcpyDeviceToHost, st), "spearman readback");
+  US_CUDA_TRY(cudaStreamSynchronize(st), "mean_row_spearman");
+  // rows i = 1 .. N-1 of every (b, h) are scored; the rest of the count is undefined
+  const long long scored = (long long)p->B * p->H * (N - 1);
+  if (defined) *defined = host_def;
+  if (undefined) *undefined = scored - host_def;
+  return US_OK;
+}
+
 us_status us_build_block_mask(const us_params* p, const float* scores, const us_selection* out,
                               void* workspace, size_t workspace_bytes, void* stream) {
   us_status s = gate(p, "build_block_mask", false);

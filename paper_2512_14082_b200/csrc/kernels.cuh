@@ -130,6 +130,16 @@ us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUte
 us_status launch_attention2(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV,
                             cudaStream_t st);
 
+// ---------------------------------------------------------------- quality metrics (metrics.cu)
+us_status launch_fill_upper(float* scores, long long planes, int N, cudaStream_t st);
+us_status launch_output_fidelity(long long rows, int d, const uint16_t* test, const uint16_t* ref, double* rows_ws,
+                                 double* out3, cudaStream_t st);
+us_status launch_block_recall(int B, int H, int N, int W, int planes, int heads_per_plane, int k,
+                              const uint32_t* mask, const float* ref, double* rows_ws, double* out,
+                              cudaStream_t st);
+us_status launch_row_spearman(int B, int H, int N, int c_h, const float* proxy, const float* ref, double* rows_ws,
+                              uint8_t* defined, double* out, long long* n_def, cudaStream_t st);
+
 // mask validation: err |= 4 for a non-causal bit, 8 for an empty causal row;
 // first offending row index (b*planes+p)*N+i recorded with atomicMin in *first_bad.
 us_status launch_mask_check(const uint32_t* mask, int rows, int N, int W, uint32_t* err,

@@ -58,6 +58,10 @@ def lib():
         _lib.or_selection_flops.argtypes = [C.c_uint64] * 4 + [C.c_int] * 4 + [C.c_uint64, C.c_void_p]
         _lib.or_rng_draws.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p]
         _lib.or_pool_sequence.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
+        _lib.or_spearman_rho.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        _lib.or_block_recall.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        _lib.or_mean_row_spearman.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                              C.c_void_p, C.c_void_p]
     return _lib
 
 
@@ -265,6 +269,42 @@ def output_fidelity(test, ref):
     out = np.zeros(3, np.float64)
     _check(lib().or_output_fidelity(_p(t), _p(r), H, L, d, _p(out)))
     return {"max_abs": out[0], "mean_rel": out[1], "cosine": out[2]}
+
+
+def spearman_rho(a, b):
+    """spearman_rho (metrics.cpp:100-116): None when one side is flat."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    if a.shape != b.shape:
+        raise OracleError("spearman_rho: length mismatch")
+    rho = np.zeros(1, np.float64)
+    d = np.zeros(1, np.int32)
+    _check(lib().or_spearman_rho(_p(a), _p(b), a.size, _p(rho), _p(d)))
+    return float(rho[0]) if d[0] else None
+
+
+def block_recall(mask, ref, k: int) -> float:
+    """block_recall (metrics.cpp:155-176): mask bool [H][N][N], ref [H][N][N]."""
+    m = np.ascontiguousarray(mask, np.uint8)
+    r = np.ascontiguousarray(ref, np.float64)
+    H, N, _ = r.shape
+    out = np.zeros(1, np.float64)
+    _check(lib().or_block_recall(_p(m), _p(r), H, N, int(k), _p(out)))
+    return float(out[0])
+
+
+def mean_row_spearman(proxy, ref, c_h: int):
+    """mean_row_spearman (metrics.cpp:201-224) -> (mean, defined, undefined)."""
+    p = np.ascontiguousarray(proxy, np.float64)
+    r = np.ascontiguousarray(ref, np.float64)
+    H, N, _ = r.shape
+    if c_h <= 0 or H % c_h != 0 or p.shape[0] != H // c_h:
+        raise OracleError("mean_row_spearman: head counts disagree")
+    mean = np.zeros(1, np.float64)
+    d = np.zeros(1, np.int64)
+    u = np.zeros(1, np.int64)
+    _check(lib().or_mean_row_spearman(_p(p), _p(r), H, N, int(c_h), _p(mean), _p(d), _p(u)))
+    return float(mean[0]), int(d[0]), int(u[0])
 
 
 def unisparse_attn(c: OrCfg, Q, K, V, nthreads=0):

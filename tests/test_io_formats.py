@@ -140,3 +140,15 @@ def test_mask_json_bytes_equal_nlohmann(tmp_path, P):
     ours = tmp_path / "ours.json"
     api.save_mask_json_bits(str(ours), _bits(m), H, N, 1, P)
     assert ours.read_bytes() == ref.read_bytes()
+
+
+def test_metrics_csv_format(tmp_path):
+    """write_metrics_csv (experiment.cpp:129-142): header and %.9g numbers."""
+    from paper_2512_14082_b200 import experiment as E
+    r = E.RunRow(proxy=1, c_q=8, c_k=8, c_h=2, strategy=2, P=0.95, causal_mode=0, rho=0.123456789012,
+                 spearman=1.0, recall=2.0 / 3.0, max_abs=1e-10, cosine=0.999999999999, selection_flops=12,
+                 attention_flops=3 * 2 ** 40)
+    E.write_metrics_csv([r], str(tmp_path / "m.csv"))
+    lines = (tmp_path / "m.csv").read_text().splitlines()
+    assert lines[0] == "proxy,c_q,c_k,c_h,strategy,P,rho,spearman,recall,max_abs,cosine,selection_flops,attention_flops"
+    assert lines[1] == "antidiagonal,8,8,2,stochastic,0.95,0.123456789,1,0.666666667,1e-10,1,12,3298534883328"

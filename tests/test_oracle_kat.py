@@ -606,3 +606,64 @@ def test_last_block_probe_single_block_and_uniform_keys():  # test_baselines.cpp
     expect = sum(32.0 / (97.0 + r) for r in range(32))
     for j in range(3):
         assert probe[0, 3, j] == pytest.approx(expect, rel=1e-9)
+
+
+# ------------------------------------------------------------------ metrics (test_metrics.cpp)
+def test_spearman_kats():  # test_metrics.cpp:28-74
+    assert O.spearman_rho([1, 2, 3, 4], [1, 3, 2, 4]) == pytest.approx(0.8, rel=1e-12)
+    assert O.spearman_rho([1, 1, 2], [1, 2, 3]) == pytest.approx(np.sqrt(3.0) / 2.0, rel=1e-12)
+    a = np.array([0.3, 1.7, -2.0, 5.5, 0.01])
+    assert O.spearman_rho(a, a) == pytest.approx(1.0, rel=1e-12)
+    assert O.spearman_rho(a, -a) == pytest.approx(-1.0, rel=1e-12)
+    assert O.spearman_rho(a, np.exp(a)) == pytest.approx(O.spearman_rho(a, a), rel=1e-12)
+    assert O.spearman_rho([2.0, 2.0, 2.0], [1.0, 2.0, 3.0]) is None
+    assert O.spearman_rho([1.0, 2.0, 3.0], [2.0, 2.0, 2.0]) is None
+    with pytest.raises(O.OracleError, match="at least 2"):
+        O.spearman_rho([1.0], [2.0])
+
+
+def _mask_rows(rows, N):
+    m = np.zeros((1, N, N), bool)
+    for i, js in enumerate(rows):
+        m[0, i, js] = True
+    return m
+
+
+def test_block_recall_kats():  # test_metrics.cpp:124-152
+    M = O.K_MASKED_SCORE
+    ref = np.array([[[5.0, M, M], [1.0, 2.0, M], [3.0, 1.0, 2.0]]])
+    m = _mask_rows([[0], [1], [0, 2]], 3)
+    assert O.block_recall(m, ref, 2) == pytest.approx(5.0 / 6.0, rel=1e-12)
+    assert O.block_recall(m, ref, 1) == pytest.approx(1.0, rel=1e-12)
+    assert O.block_recall(m, ref, 3) == pytest.approx((1.0 + 0.5 + 2.0 / 3.0) / 3.0, rel=1e-12)
+    for bad in (0, 4):
+        with pytest.raises(O.OracleError, match="k out of range"):
+            O.block_recall(m, ref, bad)
+    ref = np.array([[[1.0, M], [2.0, 2.0]]])  # ties break toward the lower index
+    assert O.block_recall(_mask_rows([[0], [0]], 2), ref, 1) == pytest.approx(1.0)
+    assert O.block_recall(_mask_rows([[0], [1]], 2), ref, 1) == pytest.approx(0.5)
+
+
+def test_mean_row_spearman_kats():  # test_metrics.cpp:164-222
+    M = O.K_MASKED_SCORE
+    rng = np.random.default_rng(3)
+    p = np.full((1, 6, 6), M)
+    for i in range(6):
+        p[0, i, :i + 1] = rng.random(i + 1)
+    mean, d, u = O.mean_row_spearman(p, p, 1)
+    assert mean == pytest.approx(1.0, rel=1e-12) and d == 5 and u == 0
+    p = np.full((1, 4, 4), M)
+    for i in range(4):
+        p[0, i, :i + 1] = rng.random(i + 1)
+    mean, d, _ = O.mean_row_spearman(p, np.concatenate([p, p]), 2)
+    assert mean == pytest.approx(1.0, rel=1e-12) and d == 6
+    with pytest.raises(O.OracleError, match="head counts disagree"):
+        O.mean_row_spearman(p, np.concatenate([p, p]), 1)
+    p = np.full((1, 3, 3), M)
+    p[0, 0, 0] = 1.0
+    p[0, 1, :2] = [0.5, 0.5]
+    p[0, 2, :3] = [0.3, 0.2, 0.1]
+    q = p.copy()
+    q[0, 1, :2] = [0.9, 0.1]
+    mean, d, u = O.mean_row_spearman(p, q, 1)
+    assert (d, u) == (1, 1) and mean == pytest.approx(1.0, rel=1e-12)
