@@ -460,6 +460,40 @@ __global__ void __launch_bounds__(384, 1)
           for (int c = 0; c < kBS; ++c)
             if (c > rloc) sv[c] = -INFINITY;
         }
+        // exponentials against a given running max (log2 units) -> packed P row, row sum
+        auto exps = [&](float m) {
+          const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+          float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                           make_float2(0.f, 0.f)};
+          if (!diag) {
+#pragma unroll
+            for (int c = 0; c < kBS; c += 2) {
+              const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+              float2 p;
+              if (c >= kPolyFrom) {
+                p = ex2_poly2(xx);
+              } else {
+                p.x = ex2_approx(xx.x);
+                p.y = ex2_approx(xx.y);
+              }
+              acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
+              packed[c >> 1] = pack_bf16(p.x, p.y);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < kBS; c += 2) {
+              const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
+              float2 p;
+              p.x = ex2_approx(xx.x);
+              p.y = ex2_approx(xx.y);
+              acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
+              packed[c >> 1] = pack_bf16(p.x, p.y);
+            }
+          }
+          const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+          const float2 s2 = __fadd2_rn(s01, s23);
+          return s2.x + s2.y;
+        };
         // 8 independent partial maxima (short dependency chains), then a tree
         float m8[8];
 #pragma unroll
@@ -495,37 +529,7 @@ __global__ void __launch_bounds__(384, 1)
           l *= f;
         }
         if (need) m_used = mx;
-        const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m_used, -m_used);
-        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                         make_float2(0.f, 0.f)};
-        if (!diag) {
-#pragma unroll
-          for (int c = 0; c < kBS; c += 2) {
-            const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
-            float2 p;
-            if (c >= kPolyFrom) {
-              p = ex2_poly2(xx);
-            } else {
-              p.x = ex2_approx(xx.x);
-              p.y = ex2_approx(xx.y);
-            }
-            acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
-            packed[c >> 1] = pack_bf16(p.x, p.y);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < kBS; c += 2) {
-            const float2 xx = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nm);
-            float2 p;
-            p.x = ex2_approx(xx.x);
-            p.y = ex2_approx(xx.y);
-            acc[(c >> 1) & 3] = __fadd2_rn(acc[(c >> 1) & 3], p);
-            packed[c >> 1] = pack_bf16(p.x, p.y);
-          }
-        }
-        const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
-        const float2 s2 = __fadd2_rn(s01, s23);
-        l += s2.x + s2.y;
+        l += exps(m_used);
       } else {
 #pragma unroll
         for (int c = 0; c < kBS / 2; ++c) packed[c] = 0u;
