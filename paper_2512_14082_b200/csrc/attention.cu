@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(384, 1)
     };
     auto issue_s = [&](int tt, int kk) {
       mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
+      if (lane == 0) TRACE(x, kk, 8);  // K/V of the step has landed
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sK = smem_u32(smem + (tt % kST) * 2 * SL::kKVBytes);
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(384, 1)
         issue_s(tn, k + 1);
       }
       mbar_wait(&bar_pfull[x], k & 1);  // P(k) is in SMEM
+      if (lane == 0) TRACE(x, k, 9);     // all four warps' P(k) stored
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sV = smem_u32(smem + (t % kST) * 2 * SL::kKVBytes + SL::kKVBytes);

@@ -33,7 +33,8 @@ eng.run(dense=not sparse); torch.cuda.synchronize()
 buf = np.zeros(2 * 4096 * 16, np.int64)
 L.us_debug_attn_trace(cta, buf.ctypes.data)
 tr = buf.reshape(2, 4096, 16)
-names = {0: "S_issue", 1: "S_seen", 4: "S_loaded", 7: "turn", 5: "math_done", 2: "P_ready", 3: "PV_issued"}
+names = {0: "S_issue", 1: "S_seen", 4: "S_loaded", 7: "turn", 5: "math_done", 2: "P_ready", 3: "PV_issued",
+         8: "KV_landed", 9: "P_all"}
 k0 = 100 if not sparse else 5
 base = tr[:, k0, 0][tr[:, k0, 0] > 0].min() if (tr[:, k0, 0] > 0).any() else 0
 for k in range(k0, k0 + 4):
@@ -50,7 +51,9 @@ for x in (0, 1):
         "seen->loaded": t[:, 4] - t[:, 1],
         "loaded->math": t[:, 5] - t[:, 4],
         "math->P": t[:, 2] - t[:, 5],
-        "P->PVissued": t[:, 3] - t[:, 2],
+        "P->Pall": t[:, 9] - t[:, 2],
+        "Pall->PVissued": t[:, 3] - t[:, 9],
+        "KVlanded->Sissue": t[:, 0] - t[:, 8],
     }
     period = np.diff(t[:, 1])
     kind = tr[x, :n - 1, 6]
