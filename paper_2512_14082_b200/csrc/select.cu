@@ -47,13 +47,12 @@ __device__ __forceinline__ int warp_sum_i32(int v) {
   return v;
 }
 
+// One row on one warp; NPL = 32-element chunks per lane held in registers (the
+// caller picks the smallest instantiation that covers the row's causal prefix,
+// so short rows do not pay for the longest one's predicated-off work).
 template <int NPL>
-__global__ void __launch_bounds__(256, 2) select_kernel(SelectArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int wpc = blockDim.x >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  for (long long row = (long long)blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows;
-       row += (long long)gridDim.x * wpc) {
+__device__ __forceinline__ void select_row(const SelectArgs& a, long long row, int lane, uint32_t lt_mask) {
+  {
     const int i = int(row % a.N);
     const int n = i + 1;
     const float* src = a.scores + row * a.N;
@@ -195,6 +194,21 @@ __global__ void __launch_bounds__(256, 2) select_kernel(SelectArgs a) {
       if (a.coverage) a.coverage[row] = cov;
       if (!certified) a.fb_rows[atomicAdd(a.fb_count, 1)] = int32_t(row);
     }
+  }
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(256, 2) select_kernel(SelectArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int wpc = blockDim.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  constexpr int kQ = NPL >= 4 ? NPL / 4 : 1, kH = NPL >= 2 ? NPL / 2 : 1;
+  for (long long row = (long long)blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows;
+       row += (long long)gridDim.x * wpc) {
+    const int n = int(row % a.N) + 1;
+    if (n <= 32 * kQ) select_row<kQ>(a, row, lane, lt_mask);
+    else if (n <= 32 * kH) select_row<kH>(a, row, lane, lt_mask);
+    else select_row<NPL>(a, row, lane, lt_mask);
   }
 }
 
