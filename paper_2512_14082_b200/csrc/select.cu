@@ -202,12 +202,13 @@ __global__ void __launch_bounds__(256, 2) select_kernel(SelectArgs a) {
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  constexpr int kQ = NPL >= 4 ? NPL / 4 : 1, kH = NPL >= 2 ? NPL / 2 : 1;
+  constexpr int kQ = NPL >= 4 ? NPL / 4 : 1, kH = NPL >= 2 ? NPL / 2 : 1, k3 = NPL >= 4 ? 3 * NPL / 4 : NPL;
   for (long long row = (long long)blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows;
        row += (long long)gridDim.x * wpc) {
     const int n = int(row % a.N) + 1;
     if (n <= 32 * kQ) select_row<kQ>(a, row, lane, lt_mask);
     else if (n <= 32 * kH) select_row<kH>(a, row, lane, lt_mask);
+    else if (n <= 32 * k3) select_row<k3>(a, row, lane, lt_mask);
     else select_row<NPL>(a, row, lane, lt_mask);
   }
 }
