@@ -87,7 +87,42 @@ __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double in
           a.src + (((long long)b * a.H_src + hs) * a.L + (long long)t * a.c) * a.d + ch * 8);
       const int stride = a.d / 8;  // uint4 per row
       float val[8];
-      if (a.strategy == US_POOL_MEAN || a.c == 1) {
+      bool done = false;
+      if (a.strategy == US_POOL_MEAN && a.c > 1 && inv_c != 0.0) {
+        // fp32 fast path: the running sum (from +0, row order, round-to-nearest) is
+        // kept only if every addition was exact (round-down == round-up), so it
+        // equals the fp64 sum; times the exact 1/c it rounds like the fp64 path
+        // (denormals included). Any inexact step (wide exponent spread, overflow,
+        // NaN) falls through to the fp64 path below.
+        float sacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        bool exact = true;
+        for (int rr = 0; rr < a.c; rr += 8) {
+          uint4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = u < a.c - rr ? ld_stream(src + (rr + u) * stride) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (u >= a.c - rr) break;
+            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xFFFF0000u);
+              exact &= __fadd_rd(sacc[2 * q], x0) == __fadd_ru(sacc[2 * q], x0);
+              exact &= __fadd_rd(sacc[2 * q + 1], x1) == __fadd_ru(sacc[2 * q + 1], x1);
+              sacc[2 * q] = __fadd_rn(sacc[2 * q], x0);
+              sacc[2 * q + 1] = __fadd_rn(sacc[2 * q + 1], x1);
+            }
+          }
+        }
+        if (exact) {
+          const float inv_cf = float(inv_c);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) val[e] = __fmul_rn(sacc[e], inv_cf);
+          done = true;
+        }
+      }
+      if (done) {
+      } else if (a.strategy == US_POOL_MEAN || a.c == 1) {
         // (c == 1 returns the window row unchanged for every strategy, compression.hpp:20)
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         int rr = 0;

@@ -61,6 +61,27 @@ def test_compress_bit_exact(c_q, c_k, c_h, H, H_kv):
         assert (Kc[b].view(np.uint32) == rk.view(np.uint32)).all()
 
 
+@pytest.mark.parametrize("c", [2, 8, 16, 64])
+def test_compress_wide_exponent_spread_bit_exact(c):
+    """Mean pooling with one element per window scaled by 10^U(-6, 4) plus signed
+    zeros, denormal-range and huge values (SURVEY §8a-1 probe 2): the fp32
+    fast path must defer every inexact window to the fp64 path."""
+    rng = np.random.default_rng(c)
+    B, H, L, d = 1, 2, 512, 64
+    Q = rng.standard_normal((B, H, L, d)).astype(np.float32)
+    Q[:, :, ::c] *= (10.0 ** rng.uniform(-6, 4, size=(B, H, L // c, d))).astype(np.float32)
+    Q[0, 0, :c] = -0.0                      # all -0 window: the sum is +0
+    Q[0, 1, :c, :8] = 1e-38                 # sums in the f32 denormal range after / c
+    Q[0, 1, c:2 * c, :8] = 3e38             # overflowing window sum (fp64 keeps it finite)
+    Q = O.bf16_round(Q)
+    K = O.bf16_round(rng.standard_normal((B, H, L, d)).astype(np.float32))
+    cfg = us().CompressionConfig(c_q=c, c_k=c, c_h=1)
+    Qc, Kc = us().compress(to_dev_bf16(Q), to_dev_bf16(K), cfg)
+    rq, rk = O.compress(O.cfg(H, L, d, 64, c_q=c, c_k=c, c_h=1), Q[0], K[0])
+    assert (Qc[0].cpu().numpy().view(np.uint32) == rq.view(np.uint32)).all()
+    assert (Kc[0].cpu().numpy().view(np.uint32) == rk.view(np.uint32)).all()
+
+
 @pytest.mark.parametrize("strategy", [1, 2])  # POOL_MAX, POOL_STOCHASTIC
 @pytest.mark.parametrize("c_q,c_k,c_h,H,H_kv", [(8, 8, 1, 8, 2), (4, 8, 2, 8, 2), (8, 8, 2, 4, 4),
                                                (64, 16, 1, 4, 1), (1, 2, 1, 2, 2)])
