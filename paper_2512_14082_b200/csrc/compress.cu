@@ -60,7 +60,10 @@ __device__ __forceinline__ double group_sum(double v, int width) {
   return __shfl_sync(0xffffffffu, v, 0, width);
 }
 
-__global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
+// STRAT: the pooling strategy, compile-time so the mean kernel (the default path)
+// carries no registers for the max / stochastic code.
+template <int STRAT>
+__global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
   const int chunks = a.d / 8;
   const int Lc = a.L / a.c;
   const long long total = (long long)a.B * a.planes * Lc * chunks;
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double in
       const int stride = a.d / 8;  // uint4 per row
       float val[8];
       bool done = false;
-      if (a.strategy == US_POOL_MEAN && a.c > 1 && inv_c != 0.0) {
+      if (STRAT == US_POOL_MEAN && a.c > 1 && inv_c != 0.0) {
         // fp32 fast path: the running sum (from +0, row order, round-to-nearest) is
         // kept only if every addition was exact (round-down == round-up), so it
         // equals the fp64 sum; times the exact 1/c it rounds like the fp64 path
@@ -122,21 +125,15 @@ __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double in
         }
       }
       if (done) {
-      } else if (a.strategy == US_POOL_MEAN || a.c == 1) {
+      } else if (STRAT == US_POOL_MEAN || a.c == 1) {
         // (c == 1 returns the window row unchanged for every strategy, compression.hpp:20)
+        // (the fp64 path: c == 1, non-power-of-two c, or a window the fp32 path
+        // could not sum exactly — rare, so one row in flight keeps registers low)
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int rr = 0;
-        for (; rr + 8 <= a.c; rr += 8) {
-          uint4 v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = ld_stream(src + (rr + u) * stride);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) bf16x8_to_f64_add(v[u], acc);
-        }
-        for (; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
+        for (int rr = 0; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
 #pragma unroll
         for (int e = 0; e < 8; ++e) val[e] = __double2float_rn(divide(acc[e], double(a.c), inv_c));
-      } else if (a.strategy == US_POOL_MAX) {
+      } else if (STRAT == US_POOL_MAX) {
         // column max over the window (compression.hpp:30-32); exact
 #pragma unroll
         for (int e = 0; e < 8; ++e) val[e] = -INFINITY;
@@ -276,7 +273,13 @@ us_status launch_compress(const CompressArgs& a, cudaStream_t st) {
   const long long total = (long long)a.B * a.planes * (a.L / a.c) * (a.d / 8);
   const int threads = 256;
   const long long blocks = (total + threads - 1) / threads;
-  compress_kernel<<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
+  if (a.strategy == US_POOL_MAX)
+    compress_kernel<US_POOL_MAX><<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
+  else if (a.strategy == US_POOL_STOCHASTIC)
+    compress_kernel<US_POOL_STOCHASTIC>
+        <<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
+  else
+    compress_kernel<US_POOL_MEAN><<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
   US_LAUNCH_CHECK("compress_kernel");
   return US_OK;
 }
