@@ -317,9 +317,17 @@ def main():
         full = gather_heads(O_loc, shards)
         torch.cuda.synchronize()
         sl = full[:, shard.q_heads.start:shard.q_heads.stop]
+        # per-rank selected blocks (max/mean bounds near-linear scaling)
+        dev = "cpu" if args.dist_backend == "gloo" else "cuda"
+        mine = torch.tensor([float(selected)], device=dev, dtype=torch.float64)
+        per_rank = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(per_rank, mine)
+        per_rank = [float(t.item()) for t in per_rank]
         gather = {"backend": dist.get_backend(), "ok": bool(torch.equal(sl, O_loc)),
                   "bytes": full.numel() * full.element_size(), "s": time.perf_counter() - t0,
-                  "head_imbalance": imbalance(shards)}
+                  "head_imbalance": imbalance(shards),
+                  "selected_blocks_per_rank": [int(x) for x in per_rank],
+                  "selected_imbalance": max(per_rank) / (sum(per_rank) / world) if sum(per_rank) else 1.0}
         del full, sl
 
     # ---------------------------------------------------------------- dense baselines (same shard)
