@@ -434,11 +434,18 @@ class Engine:
             kv0 += n
         return plan
 
-    def run_host(self, Qh, Kh, Vh, Oh, chunks: int = 4):
+    def run_host(self, Qh, Kh, Vh, Oh, chunks: int = 4, wait: bool = True):
         """unisparse_attn from (pinned) host buffers: H2D of Q/K/V, the hot path,
         D2H of O, pipelined over KV-head chunks on three CUDA streams (copy-in,
         compute, copy-out) so the PCIe transfers overlap the kernels. Enqueues
-        only; returns the event recorded after the last D2H on the copy-out stream."""
+        only; returns the event recorded after the last D2H on the copy-out stream.
+
+        wait=True: the current stream waits for that event (the call is ordered
+        like any other stream op). wait=False: it does not, so back-to-back calls
+        overlap — call n+1 copies chunk c in as soon as call n has computed chunk
+        c, and computes chunk c once call n's copy-out of chunk c is done (the
+        per-chunk hazards on the engine's device buffers); the caller waits on
+        the returned event before reading Oh or ordering later work."""
         plan = self._chunk_plan(chunks) if chunks > 1 else None
         cur = torch.cuda.current_stream()
         if not hasattr(self, "_streams"):
@@ -448,6 +455,12 @@ class Engine:
         start.record(cur)
         for s_ in self._streams:
             s_.wait_event(start)
+        prev = getattr(self, "_chunk_events", None)
+        if prev is not None and (plan is None or len(prev[1]) != len(plan)):
+            for s_ in self._streams:  # a different chunking: order after the whole previous call
+                s_.wait_event(prev[0])
+            prev = None
+        self._chunk_events = None
         if plan is None:
             with torch.cuda.stream(s_comp):
                 self.Q.copy_(Qh, non_blocking=True)
@@ -457,18 +470,25 @@ class Engine:
                 Oh.copy_(self.O, non_blocking=True)
             done = torch.cuda.Event()
             done.record(s_comp)
-            cur.wait_event(done)
+            if wait:
+                cur.wait_event(done)
+            self._chunk_events = (done, [])
             return done
         G = self.p.H // self.p.H_kv
         ws = _ptr(self.ws)
-        for cp, (q0, q1), (k0, k1), sel in plan:
-            e_in, e_comp = torch.cuda.Event(), torch.cuda.Event()
+        events = []
+        for c, (cp, (q0, q1), (k0, k1), sel) in enumerate(plan):
+            e_in, e_comp, e_out = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
+            if prev is not None:
+                s_in.wait_event(prev[1][c][0])    # the previous call has consumed Q/K/V chunk c
             with torch.cuda.stream(s_in):
                 self.Q[:, q0:q1].copy_(Qh[:, q0:q1], non_blocking=True)
                 self.K[:, k0:k1].copy_(Kh[:, k0:k1], non_blocking=True)
                 self.V[:, k0:k1].copy_(Vh[:, k0:k1], non_blocking=True)
                 e_in.record(s_in)
             s_comp.wait_event(e_in)
+            if prev is not None:
+                s_comp.wait_event(prev[1][c][1])  # ... and copied O chunk c out
             _raise(lib().us_unisparse_attention(
                 C.byref(cp), _ptr(self.Q[:, q0:q1]), _ptr(self.K[:, k0:k1]), _ptr(self.V[:, k0:k1]),
                 _ptr(self.O[:, q0:q1]), _ptr(self.lse[:, q0:q1]), C.byref(sel), ws, self.ws.numel(),
@@ -477,9 +497,13 @@ class Engine:
             s_out.wait_event(e_comp)
             with torch.cuda.stream(s_out):
                 Oh[:, q0:q1].copy_(self.O[:, q0:q1], non_blocking=True)
+                e_out.record(s_out)
+            events.append((e_comp, e_out))
         done = torch.cuda.Event()
         done.record(s_out)
-        cur.wait_event(done)
+        if wait:
+            cur.wait_event(done)
+        self._chunk_events = (done, events)
         return done
 
 
