@@ -184,16 +184,22 @@ def _check_inputs(*ts: torch.Tensor):
 
 
 # ------------------------------------------------------------------ workspace cache
+# Workspaces are reused in stream order, so the cache is keyed by (device, stream):
+# calls on different streams (or host threads using different streams) never share one.
 _ws_cache: dict = {}
+
+
+def _ws_key():
+    return (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
 
 
 def workspace(p: UsParams) -> torch.Tensor:
     need = lib().us_workspace_bytes(C.byref(p))
-    dev = torch.cuda.current_device()
-    cur = _ws_cache.get(dev)
+    key = _ws_key()
+    cur = _ws_cache.get(key)
     if cur is None or cur.numel() < need:
-        cur = torch.empty(max(need, 256), dtype=torch.uint8, device=f"cuda:{dev}")
-        _ws_cache[dev] = cur
+        cur = torch.empty(max(need, 256), dtype=torch.uint8, device=f"cuda:{key[0]}")
+        _ws_cache[key] = cur
     return cur
 
 
@@ -308,7 +314,7 @@ def select_blocks(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: i
     ws = workspace(p)
     if ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=Q.device)
-        _ws_cache[torch.cuda.current_device()] = ws
+        _ws_cache[_ws_key()] = ws
     sel = _alloc_selection(p, with_scores, with_indices)
     ss = _sel_struct(sel)
     _raise(lib().us_select_proxy(C.byref(p), proxy, stride, _ptr(Q), _ptr(K), C.byref(ss), _ptr(ws), ws.numel(),
