@@ -54,6 +54,64 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clock + clock-event (throttle) reasons sampled every 10 ms through NVML
+    (nvidia-ml-py) during the timed region; `ClockSampler` (nvidia-smi, 200 ms) is
+    the fallback when NVML is unavailable."""
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, index: int):
+        import pynvml
+        pynvml.nvmlInit()
+        self.n = pynvml
+        self.h = None
+        try:  # the CUDA ordinal -> NVML handle through the PCI bus id (CUDA_VISIBLE_DEVICES-proof)
+            import torch
+            pr = torch.cuda.get_device_properties(index)
+            bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+
+    def _run(self):
+        n = self.n
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM))
+                mask = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.NAMES:
+                    if mask & getattr(n, attr, 0):
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001 - a failed query ends sampling, not the bench
+                break
+            self.stop_ev.wait(0.01)
+
+    def start(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join(timeout=1)
+        try:
+            mx = self.n.nvmlDeviceGetMaxClockInfo(self.h, self.n.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            mx = None
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": mx,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml, 10 ms"}
+
+
+def clock_sampler(index: int):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:  # noqa: BLE001 - no NVML: nvidia-smi polling
+        return ClockSampler(index)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -264,7 +322,7 @@ def main():
     # ---------------------------------------------------------------- timed region (device)
     stream = torch.cuda.current_stream()
     us.api.profile_enable(args.steps)
-    clocks = ClockSampler(local)
+    clocks = clock_sampler(local)
     clocks.start()
     barrier()
     torch.cuda.synchronize()
