@@ -54,13 +54,15 @@
 #if US_ATTN_TRACE
 __device__ long long g_attn_trace[2 * 4096 * 16];
 __device__ int g_attn_trace_cta;
+// (us_traced is computed once per thread at kernel entry: a per-event global load of
+// g_attn_trace_cta cost the tracing warps hundreds of cycles per step)
 #define TRACE(x, k, e)                                                                  \
   do {                                                                                  \
-    if (blockIdx.x == g_attn_trace_cta && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 16 + (e)] = clock64(); \
+    if (us_traced && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 16 + (e)] = clock64(); \
   } while (0)
 #define TRACEV(x, k, e, v)                                                              \
   do {                                                                                  \
-    if (blockIdx.x == g_attn_trace_cta && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 16 + (e)] = (v); \
+    if (us_traced && (k) < 4096) g_attn_trace[((x) * 4096 + (k)) * 16 + (e)] = (v); \
   } while (0)
 #else
 #define TRACEV(x, k, e, v) \
@@ -187,6 +189,9 @@ __global__ void __launch_bounds__(384, 1)
   __shared__ uint32_t steps[kMaxN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if US_ATTN_TRACE
+  const bool us_traced = blockIdx.x == g_attn_trace_cta;
+#endif
   const int G = a.H / a.H_kv;
   const Groups gr = decode_item(a, blockIdx.x);
   const int kvh = gr.h[0] / G;
@@ -547,6 +552,7 @@ __global__ void __launch_bounds__(384, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (row == 0) TRACE(x, k, 2);
+      if (lane == 0) TRACE(x, k, 10 + q);  // this warp's P(k) hand-off
       if (lane == 0) mbar_arrive(&bar_pfull[x]);
       ++k;
     }

@@ -64,3 +64,14 @@ for x in (0, 1):
                   ", ".join(f"{k} {v[:-1][sel].mean():.0f}" for k, v in ph.items()))
     print(f"tile {'AB'[x]}: {n} steps, mean period {period.mean():.0f} cycles; " +
           ", ".join(f"{k} {v[1:].mean():.0f}" for k, v in ph.items()))
+    # per-warp P hand-off (slots 10-13): which lane quarter arrives last, and by how much
+    pw = t[:, 10:14]
+    ok = (pw > 0).all(1)
+    if ok.any():
+        pw = pw[ok]
+        last = pw.argmax(1)
+        spread = pw.max(1) - pw.min(1)
+        print(f"  tile {'AB'[x]} per-warp P hand-off: mean spread {spread.mean():.0f} cycles; last warp (quarter) histogram "
+              + str(np.bincount(last, minlength=4).tolist())
+              + "; mean lag behind the first warp per quarter "
+              + str([int(v) for v in (pw - pw.min(1, keepdims=True)).mean(0)]))
