@@ -20,7 +20,8 @@
 // group's output equals sparse attention over exactly its own selection.
 //
 // Roles (384 threads): warp 0 TMA producer (5-stage K/V ring), warps 1 / 3
-// MMA issuers of tile A / B (warp 1 owns TMEM), warp 2 builds the union list,
+// MMA issuers of tile A / B (warp 1 owns TMEM), warp 2 builds the union list
+// (uint16 entries: block | slot bits << 12) and each tile's own-step list,
 // warps 4-7 softmax of tile A, warps 8-11 softmax of tile B (thread = row).
 // TMEM per tile X (256 cols at X*256): S [0,64) fp32, O [64,192), Q [192,256)
 // (bf16x2, A operand of S = Q K^T, TS-mode MMA). P (bf16) goes to a
@@ -185,8 +186,11 @@ __global__ void __launch_bounds__(384, 1)
   __shared__ int n_steps_sh;
   __shared__ uint32_t perm_sh;  // group of tile slot s = (perm_sh >> 2s) & 3
   __shared__ uint32_t mrow[4][kMaxW];
-  // union of the four groups' selected blocks, ascending: j | sel_slot << (16 + slot)
-  __shared__ uint32_t steps[kMaxN];
+  // union of the four groups' selected blocks, ascending: j | sel_slot << (12 + slot)
+  __shared__ uint16_t steps[kMaxN];
+  // per tile: the union positions it computes (its own steps), ascending
+  __shared__ uint16_t own_pos[2][kMaxN];
+  __shared__ int n_own_sh[2];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if US_ATTN_TRACE
@@ -281,10 +285,24 @@ __global__ void __launch_bounds__(384, 1)
         u &= u - 1u;
         uint32_t e = uint32_t((w << 5) + bit);
 #pragma unroll
-        for (int g = 0; g < 4; ++g) e |= ((m[g] >> bit) & 1u) << (16 + g);
-        steps[pos++] = e;
+        for (int g = 0; g < 4; ++g) e |= ((m[g] >> bit) & 1u) << (12 + g);
+        steps[pos++] = uint16_t(e);
       }
       base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    // own-step lists of the two tiles (the softmax warps walk only their own steps)
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      int n = 0;
+      for (int t0 = 0; t0 < base; t0 += 32) {
+        const int t = t0 + lane;
+        const bool mine = t < base && ((steps[t] >> (12 + 2 * x)) & 3u) != 0u;
+        const uint32_t b = __ballot_sync(0xffffffffu, mine);
+        if (mine) own_pos[x][n + __popc(b & ((1u << lane) - 1u))] = uint16_t(t);
+        n += __popc(b);
+      }
+      if (lane == 0) n_own_sh[x] = n;
     }
     if (lane == 0) {
       n_steps_sh = base;
@@ -305,7 +323,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t pol_kv = policy_evict_last();
       const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
       for (int t = 0; t < T; ++t) {
-        const int j = int(steps[t] & 0xFFFFu);
+        const int j = int(steps[t] & 0xFFFu);
         const int s = t % kST;
         if (t >= kST) mbar_wait(&bar_kvempty[s], ((t / kST) + 1) & 1);
         uint8_t* sk = smem + s * 2 * SL::kKVBytes;
@@ -325,12 +343,9 @@ __global__ void __launch_bounds__(384, 1)
     constexpr uint32_t idesc_o = idesc_f16(128, D, /*bf16*/ 1, false, /*V MN-major*/ true);
     const uint32_t tb = tmem + x * 256;
     const uint32_t sP = smem_u32(smem + SL::kRingBytes + x * SL::kPBytes);
-    auto own = [&](int tt) { return ((steps[tt] >> (16 + 2 * x)) & 3u) != 0u; };
-    auto next_own = [&](int from) {
-      int tt = from;
-      while (tt < T && !own(tt)) ++tt;
-      return tt;
-    };
+    const int n_own = n_own_sh[x];
+    // union position of own step kk (T past the last)
+    auto own_at = [&](int kk) { return kk < n_own ? int(own_pos[x][kk]) : T; };
     // Release union positions [from, to) this tile skips. Waiting for each tile to
     // land keeps this warp's kv_empty arrivals in phase order (one per stage phase).
     auto release = [&](int from, int to) {
@@ -359,12 +374,12 @@ __global__ void __launch_bounds__(384, 1)
     };
     mbar_wait(&bar_q[x], 0);  // Q rows of tile x are in TMEM
     tc_fence_after();
-    int t = next_own(0);
+    int t = own_at(0);
     release(0, t);
     if (t < T) issue_s(t, 0);
     int k = 0;
     while (t < T) {
-      const int tn = next_own(t + 1);
+      const int tn = own_at(k + 1);
       const bool early = tn < T && tn - t < kST;
       mbar_wait(&bar_sfree[x], k & 1);  // the softmax has loaded S(k): S columns are free
       if (early) {
@@ -433,15 +448,15 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0) mbar_arrive(&bar_q[x]);
     }
     int k = 0;
-    for (int t = 0; t < T; ++t) {
-      const uint32_t e = steps[t];
-      if (((e >> (16 + 2 * x)) & 3u) == 0u) continue;  // not a step of this tile
-      const int j = int(e & 0xFFFFu);
-      const bool sel = (e >> (16 + slot)) & 1u;
+    const int n_own = n_own_sh[x];
+    for (int kk = 0; kk < n_own; ++kk) {
+      const uint32_t e = steps[own_pos[x][kk]];
+      const int j = int(e & 0xFFFu);
+      const bool sel = (e >> (12 + slot)) & 1u;
       mbar_wait(&bar_sfull[x], k & 1);
       tc_fence_after();
       if (row == 0) TRACE(x, k, 1);
-      if (row == 0) TRACEV(x, k, 6, (long long)((e >> (16 + 2 * x)) & 3u));  // step kind
+      if (row == 0) TRACEV(x, k, 6, (long long)((e >> (12 + 2 * x)) & 3u));  // step kind
       float sv[kBS];
       if (sel) {
         uint32_t v[32], v2[32];
