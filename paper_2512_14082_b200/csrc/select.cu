@@ -202,13 +202,22 @@ __global__ void __launch_bounds__(256, 2) select_kernel(SelectArgs a) {
   const int lane = threadIdx.x & 31;
   const int wpc = blockDim.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  constexpr int kQ = NPL >= 4 ? NPL / 4 : 1, kH = NPL >= 2 ? NPL / 2 : 1, k3 = NPL >= 4 ? 3 * NPL / 4 : NPL;
+  // eighths of the longest row (quarters / halves / whole for short N)
+  constexpr int E = NPL >= 8 ? NPL / 8 : 1;
   for (long long row = (long long)blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows;
        row += (long long)gridDim.x * wpc) {
     const int n = int(row % a.N) + 1;
-    if (n <= 32 * kQ) select_row<kQ>(a, row, lane, lt_mask);
-    else if (n <= 32 * kH) select_row<kH>(a, row, lane, lt_mask);
-    else if (n <= 32 * k3) select_row<k3>(a, row, lane, lt_mask);
+    if (NPL < 8) {
+      if (n <= 32 * (NPL >= 4 ? NPL / 4 : 1)) select_row<(NPL >= 4 ? NPL / 4 : 1)>(a, row, lane, lt_mask);
+      else if (n <= 32 * (NPL >= 2 ? NPL / 2 : 1)) select_row<(NPL >= 2 ? NPL / 2 : 1)>(a, row, lane, lt_mask);
+      else select_row<NPL>(a, row, lane, lt_mask);
+    } else if (n <= 32 * E) select_row<E>(a, row, lane, lt_mask);
+    else if (n <= 64 * E) select_row<2 * E>(a, row, lane, lt_mask);
+    else if (n <= 96 * E) select_row<3 * E>(a, row, lane, lt_mask);
+    else if (n <= 128 * E) select_row<4 * E>(a, row, lane, lt_mask);
+    else if (n <= 160 * E) select_row<5 * E>(a, row, lane, lt_mask);
+    else if (n <= 192 * E) select_row<6 * E>(a, row, lane, lt_mask);
+    else if (n <= 224 * E) select_row<7 * E>(a, row, lane, lt_mask);
     else select_row<NPL>(a, row, lane, lt_mask);
   }
 }
