@@ -187,6 +187,15 @@ us_status us_output_fidelity(const us_params* p, const void* O_test, const void*
 us_status us_block_recall(const us_params* p, const uint32_t* mask_bits, int32_t heads_per_plane, const float* ref,
                           int32_t k, double* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* planted_recall (metrics.cpp:178-199): the mean over (b, h, i) rows with a
+ * non-empty planted list of the fraction of planted blocks the mask selected;
+ * planted int32 [B][H][N][m], -1 = unused slot (the generator's planted sets,
+ * workloads.cpp:98-125). US_ERR_INVALID_ARGUMENT "planted_recall: no planted rows"
+ * when every list is empty. */
+us_status us_planted_recall(const us_params* p, const uint32_t* mask_bits, int32_t heads_per_plane,
+                            const int32_t* planted, int32_t m, double* out, void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* mean_row_spearman (metrics.cpp:201-224): proxy scores f32 [B][H/c_h][N][N]
  * (c_h = p->c_h) against ref f32 [B][H][N][N], rows i >= 1; flat rows count as
  * undefined. */

@@ -893,6 +893,28 @@ int or_block_recall(const uint8_t* mask, const double* ref, int H, int N, int k,
   return 0;
 }
 
+// planted_recall (metrics.cpp:178-199): mask [H][N][N] bytes, planted [H][N][m] (-1 = none).
+int or_planted_recall(const uint8_t* mask, const int32_t* planted, int H, int N, int m, double* out) {
+  double sum = 0.0;
+  int64_t rows = 0;
+  for (int h = 0; h < H; ++h)
+    for (int i = 0; i < N; ++i) {
+      int want = 0, hit = 0;
+      for (int t = 0; t < m; ++t) {
+        const int j = planted[(size_t(h) * N + i) * m + t];
+        if (j < 0) continue;
+        ++want;
+        hit += mask[(size_t(h) * N + i) * N + j] ? 1 : 0;
+      }
+      if (want == 0) continue;
+      sum += double(hit) / double(want);
+      ++rows;
+    }
+  if (rows == 0) return fail("planted_recall: no planted rows");
+  *out = sum / double(rows);
+  return 0;
+}
+
 // mean_row_spearman (metrics.cpp:201-224): proxy [H/c_h][N][N], reference [H][N][N].
 int or_mean_row_spearman(const double* proxy, const double* ref, int H, int N, int c_h, double* mean,
                          int64_t* defined, int64_t* undefined) {

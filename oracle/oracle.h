@@ -133,6 +133,7 @@ int or_output_fidelity(const float* test, const float* ref, int H, int L, int d_
 /* metrics.cpp:100-224 — spearman_rho (average ranks), block_recall, mean_row_spearman */
 int or_spearman_rho(const double* a, const double* b, int n, double* rho, int* defined);
 int or_block_recall(const uint8_t* mask, const double* ref, int H, int N, int k, double* out);
+int or_planted_recall(const uint8_t* mask, const int32_t* planted, int H, int N, int m, double* out);
 int or_mean_row_spearman(const double* proxy, const double* ref, int H, int N, int c_h, double* mean,
                          int64_t* defined, int64_t* undefined);
 int or_unisparse_attn(const or_cfg* cfg, const float* Q, const float* K, const float* V,

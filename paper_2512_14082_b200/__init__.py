@@ -10,7 +10,7 @@ from .api import (  # noqa: F401
     InvalidMaskError, CudaError, block_sparse_attention, build_block_mask, compress,
     dense_attention, select_blocks, selection_flops, unisparse_attn, make_params, validate,
     POOL_MEAN, POST_SOFTMAX_BLOCK_CAUSAL, PRE_SOFTMAX_COMPRESSED_CAUSAL, SELECT_TOP_P, SELECT_TOP_K,
-    exact_block_mass, output_fidelity, block_recall, mean_row_spearman,
+    exact_block_mass, output_fidelity, block_recall, mean_row_spearman, planted_recall,
 )
 
 __version__ = "0.1.0"

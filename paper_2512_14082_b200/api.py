@@ -130,6 +130,7 @@ def lib() -> C.CDLL:
             L.us_output_fidelity.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
             L.us_block_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
             L.us_mean_row_spearman.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+            L.us_planted_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
         return _lib
 
 
@@ -656,3 +657,22 @@ def mean_row_spearman(proxy: torch.Tensor, ref: torch.Tensor, c_h: int, S: int =
     _raise(lib().us_mean_row_spearman(C.byref(p), _ptr(proxy.float().contiguous()), _ptr(ref.float().contiguous()),
                                       C.byref(mean), C.byref(d), C.byref(u), _ptr(ws), ws.numel(), _stream()))
     return mean.value, d.value, u.value
+
+
+def planted_recall(mask_bits: torch.Tensor, planted: torch.Tensor, heads_per_plane: int = 1, S: int = 64) -> float:
+    """planted_recall (metrics.cpp:178-199): mask planes int32 [B, planes, N, W] against
+    planted block lists int32 [B, H, N, m] (-1 = unused slot)."""
+    if planted.dim() == 3:
+        planted = planted.unsqueeze(0)
+    if mask_bits.dim() == 3:
+        mask_bits = mask_bits.unsqueeze(0)
+    B, H, N, m = planted.shape
+    if mask_bits.shape[1] * heads_per_plane != H:
+        raise ValueError("planted_recall: planted must hold one list set per head")
+    p = _metric_params(B, H, N * S, 64, S)
+    ws = _scratch(lib().us_metrics_workspace_bytes(C.byref(p)), planted.device)
+    out = C.c_double(0.0)
+    _raise(lib().us_planted_recall(C.byref(p), _ptr(mask_bits.contiguous()), heads_per_plane,
+                                   _ptr(planted.to(torch.int32).contiguous()), m, C.byref(out), _ptr(ws), ws.numel(),
+                                   _stream()))
+    return out.value

@@ -735,6 +735,37 @@ us_status us_block_recall(const us_params* p, const uint32_t* mask_bits, int32_t
   return US_OK;
 }
 
+us_status us_planted_recall(const us_params* p, const uint32_t* mask_bits, int32_t heads_per_plane,
+                            const int32_t* planted, int32_t m, double* out, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  us_status s = gate(p, "planted_recall", false);
+  if (s != US_OK) return s;
+  if (!planted || m <= 0 || !mask_bits || !out || heads_per_plane <= 0 || p->H % heads_per_plane != 0) {
+    set_error("planted_recall: planted must hold one list set per head");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  if ((s = metrics_ws(p, workspace, workspace_bytes, "planted_recall")) != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int N = p->L / p->S;
+  const long long rows = (long long)p->B * p->H * N;
+  double* res = at<double>(workspace, 0);
+  long long* ndef = at<long long>(workspace, 64);
+  double* row_val = at<double>(workspace, 256);
+  uint8_t* def = reinterpret_cast<uint8_t*>(row_val + rows);
+  if ((s = launch_planted_recall(p->B, p->H, N, (N + 31) / 32, p->H / heads_per_plane, heads_per_plane, m, mask_bits,
+                                 planted, row_val, def, res, ndef, st)) != US_OK)
+    return s;
+  long long host_def = 0;
+  US_CUDA_TRY(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, st), "planted readback");
+  US_CUDA_TRY(cudaMemcpyAsync(&host_def, ndef, sizeof(long long), cudaMemcpyDeviceToHost, st), "planted readback");
+  US_CUDA_TRY(cudaStreamSynchronize(st), "planted_recall");
+  if (host_def == 0) {
+    set_error("planted_recall: no planted rows");
+    return US_ERR_INVALID_ARGUMENT;
+  }
+  return US_OK;
+}
+
 us_status us_mean_row_spearman(const us_params* p, const float* proxy, const float* ref, double* mean,
                                int64_t* defined, int64_t* undefined, void* workspace, size_t workspace_bytes,
                                void* stream) {

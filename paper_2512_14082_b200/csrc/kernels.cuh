@@ -132,6 +132,9 @@ us_status launch_attention2(const AttnArgs& a, const CUtensorMap& tmK, const CUt
 
 // ---------------------------------------------------------------- quality metrics (metrics.cu)
 us_status launch_fill_upper(float* scores, long long planes, int N, cudaStream_t st);
+us_status launch_planted_recall(int B, int H, int N, int W, int planes, int heads_per_plane, int m,
+                                const uint32_t* mask, const int32_t* planted, double* rows_ws, uint8_t* defined,
+                                double* out, long long* n_def, cudaStream_t st);
 us_status launch_output_fidelity(long long rows, int d, const uint16_t* test, const uint16_t* ref, double* rows_ws,
                                  double* out3, cudaStream_t st);
 us_status launch_block_recall(int B, int H, int N, int W, int planes, int heads_per_plane, int k,

@@ -275,6 +275,30 @@ __global__ void __launch_bounds__(kThreads) spearman_rows_kernel(const SpearmanA
   }
 }
 
+// ---------------------------------------------------------------- planted_recall
+// metrics.cpp:178-199: per (b, h, i) with a non-empty planted list, the fraction of
+// planted blocks the mask selected; planted = int32 [B][H][N][m], -1 = unused slot.
+__global__ void planted_rows_kernel(int B, int H, int N, int W, int planes, int heads_per_plane, int m,
+                                    const uint32_t* __restrict__ mask, const int32_t* __restrict__ planted,
+                                    double* __restrict__ row_val, uint8_t* __restrict__ defined) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long long)B * H * N) return;
+  const int i = int(r % N);
+  const long long bh = r / N;
+  const int b = int(bh / H), h = int(bh % H);
+  const uint32_t* mrow = mask + ((long long)(b * planes + h / heads_per_plane) * N + i) * W;
+  const int32_t* want = planted + r * m;
+  int w = 0, hit = 0;
+  for (int t = 0; t < m; ++t) {
+    const int j = want[t];
+    if (j < 0 || j >= N) continue;
+    ++w;
+    hit += (mrow[j >> 5] >> (j & 31)) & 1u;
+  }
+  defined[r] = w > 0;
+  row_val[r] = w > 0 ? double(hit) / double(w) : 0.0;
+}
+
 // kMaskedScore (types.hpp:32) above the diagonal of [planes][N][N] block scores
 __global__ void fill_upper_kernel(float* s, int N) {
   const int i = blockIdx.x % N;
@@ -289,6 +313,18 @@ constexpr size_t kSpearmanSmem = size_t(kMaxN) * (8 + 8 + 8 + 4);
 us_status launch_fill_upper(float* scores, long long planes, int N, cudaStream_t st) {
   fill_upper_kernel<<<unsigned(planes * N), 128, 0, st>>>(scores, N);
   US_LAUNCH_CHECK("fill_upper_kernel");
+  return US_OK;
+}
+
+us_status launch_planted_recall(int B, int H, int N, int W, int planes, int heads_per_plane, int m,
+                                const uint32_t* mask, const int32_t* planted, double* rows_ws, uint8_t* defined,
+                                double* out, long long* n_def, cudaStream_t st) {
+  const long long rows = (long long)B * H * N;
+  planted_rows_kernel<<<unsigned((rows + 255) / 256), 256, 0, st>>>(B, H, N, W, planes, heads_per_plane, m, mask,
+                                                                    planted, rows_ws, defined);
+  US_LAUNCH_CHECK("planted_rows_kernel");
+  ordered_mean_kernel<<<1, 32, 0, st>>>(rows, rows_ws, defined, out, n_def);
+  US_LAUNCH_CHECK("ordered_mean_kernel");
   return US_OK;
 }
 

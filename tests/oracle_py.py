@@ -60,6 +60,7 @@ def lib():
         _lib.or_pool_sequence.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
         _lib.or_spearman_rho.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         _lib.or_block_recall.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        _lib.or_planted_recall.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         _lib.or_mean_row_spearman.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                               C.c_void_p, C.c_void_p]
     return _lib
@@ -290,6 +291,16 @@ def block_recall(mask, ref, k: int) -> float:
     H, N, _ = r.shape
     out = np.zeros(1, np.float64)
     _check(lib().or_block_recall(_p(m), _p(r), H, N, int(k), _p(out)))
+    return float(out[0])
+
+
+def planted_recall(mask, planted) -> float:
+    """planted_recall (metrics.cpp:178-199): mask bool [H][N][N], planted int [H][N][m] (-1 = none)."""
+    mk = np.ascontiguousarray(mask, np.uint8)
+    pl = np.ascontiguousarray(planted, np.int32)
+    H, N, m = pl.shape
+    out = np.zeros(1, np.float64)
+    _check(lib().or_planted_recall(_p(mk), _p(pl), H, N, m, _p(out)))
     return float(out[0])
 
 

@@ -205,3 +205,21 @@ def test_run_experiment_writes_reference_files(tmp_path):
     assert rows[0].cosine > 0.9
     with pytest.raises(E.ValidationError, match="stride must divide S"):
         E.run_experiment(q, k, v, grid=grid, proxies=(1,), stride=3)
+
+
+def test_planted_recall_on_gpu():  # test_metrics.cpp:154-161 and the generator's planted sets
+    m = np.zeros((1, 3, 3), bool)
+    for i, js in enumerate([[0], [0, 1], [0, 2]]):
+        m[0, i, js] = True
+    planted = torch.tensor([[[-1, -1], [0, -1], [1, 2]]], dtype=torch.int32).cuda()
+    bits = torch.from_numpy(_bits(m)).cuda()
+    assert us().planted_recall(bits, planted) == pytest.approx(0.75, rel=1e-12)
+    with pytest.raises(ValueError, match="no planted rows"):
+        us().planted_recall(bits, torch.full((1, 3, 2), -1, dtype=torch.int32).cuda())
+    # the planted workload through the GPU pipeline: equal to the oracle on the same mask
+    L, H, H_kv, d = 4096, 4, 2, 64
+    Q, K, V, pl = workload(O.WL_PLANTED, L, H, H_kv, d, 23)
+    rep = us().select_blocks(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), us().CompressionConfig(P=0.9))
+    got = us().planted_recall(rep.mask.mask_bits, torch.from_numpy(pl).cuda())
+    want = O.planted_recall(rep.mask.dense_mask(H)[0].cpu().numpy(), pl)
+    assert got == want and got > 0.5

@@ -667,3 +667,11 @@ def test_mean_row_spearman_kats():  # test_metrics.cpp:164-222
     q[0, 1, :2] = [0.9, 0.1]
     mean, d, u = O.mean_row_spearman(p, q, 1)
     assert (d, u) == (1, 1) and mean == pytest.approx(1.0, rel=1e-12)
+
+
+def test_planted_recall_kats():  # test_metrics.cpp:154-161
+    m = _mask_rows([[0], [0, 1], [0, 2]], 3)
+    planted = np.array([[[-1, -1], [0, -1], [1, 2]]], np.int32)
+    assert O.planted_recall(m, planted) == pytest.approx(0.75, rel=1e-12)
+    with pytest.raises(O.OracleError, match="no planted rows"):
+        O.planted_recall(m, np.full((1, 3, 2), -1, np.int32))
