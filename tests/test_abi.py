@@ -75,3 +75,33 @@ def test_cpp_wrapper_gpu():
     r = subprocess.run([WRAPPER, "gpu"], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_acceptance_criterion_7_flop_identities(lib):
+    """acceptance.cpp criterion 7 through us_selection_flops (host arithmetic, no
+    GPU): compressed_qk * c_q * c_k * c_h == 2 L^2 H d exactly, dense = 2x that,
+    c_h = 2 halves the compressed scoring and aggregation terms (S = 64 here; the
+    reference battery uses S = 128, every identity is S-independent)."""
+    from paper_2512_14082_b200.api import UsParams
+    lib.us_selection_flops.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, C.c_void_p]
+    out = (C.c_uint64 * 6)()
+    ok = True
+    for L in (1024, 2048, 4096):
+        for H in (2, 4, 8):
+            for d in (64, 128):
+                dense_qk = 2 * L * L * H * d
+                for c_q in (1, 2, 4, 8, 16, 32, 64):
+                    for c_k in (1, 4, 8, 64):
+                        for c_h in (1, 2):
+                            p = UsParams(1, H, H, L, d, 64, c_q, c_k, c_h, 0, 0, 0, 0.95, 0, 0, 0)
+                            assert lib.us_selection_flops(C.byref(p), 0, 8, C.cast(out, C.c_void_p)) == 0
+                            qk, dense = out[1], out[5]
+                            ok &= qk * c_q * c_k * c_h == dense_qk and dense_qk % qk == 0
+                            ok &= dense == 2 * dense_qk
+                f = []
+                for c_h in (1, 2):
+                    p = UsParams(1, H, H, L, d, 64, 8, 8, c_h, 0, 0, 0, 0.95, 0, 0, 0)
+                    lib.us_selection_flops(C.byref(p), 0, 8, C.cast(out, C.c_void_p))
+                    f.append((out[1], out[2]))
+                ok &= f[0][0] == 2 * f[1][0] and f[0][1] == 2 * f[1][1]
+    assert ok
