@@ -223,3 +223,47 @@ def test_planted_recall_on_gpu():  # test_metrics.cpp:154-161 and the generator'
     got = us().planted_recall(rep.mask.mask_bits, torch.from_numpy(pl).cuda())
     want = O.planted_recall(rep.mask.dense_mask(H)[0].cpu().numpy(), pl)
     assert got == want and got > 0.5
+
+
+def _small_inputs(seed=5):
+    Q, K, V, _ = workload(O.WL_PLANTED, 2048, 2, 2, 64, seed)
+    return to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1)
+
+
+def test_run_experiment_p1_rows_are_dense_and_grid_order():  # test_experiment.cpp:99-133
+    from paper_2512_14082_b200 import experiment as E
+    q, k, v = _small_inputs()
+    rows = E.run_experiment(q, k, v, grid=E.Grid(P=(0.9, 1.0)), proxies=(0, 2))
+    assert [(r.P, r.proxy) for r in rows] == [(0.9, 0), (0.9, 2), (1.0, 0), (1.0, 2)]
+    for r in rows[2:]:
+        assert r.rho == 0.0 and r.max_abs == 0.0 and r.cosine >= 1.0 - 1e-9
+    assert rows[0].rho > 0.0
+
+
+def test_run_experiment_coarser_compression_cuts_selection_flops():  # test_experiment.cpp:135-144
+    from paper_2512_14082_b200 import experiment as E
+    q, k, v = _small_inputs()
+    rows = E.run_experiment(q, k, v, grid=E.Grid(c_q=(1, 2, 4, 8), c_k=(4,)))
+    assert all(rows[i].selection_flops < rows[i - 1].selection_flops for i in range(1, 4))
+
+
+def test_run_experiment_rejects_inconsistent_grids_upfront(tmp_path):  # test_experiment.cpp:85-97
+    from paper_2512_14082_b200 import experiment as E
+    q, k, v = _small_inputs()
+    with pytest.raises(E.ValidationError, match="not divisible by c_q=48"):
+        E.run_experiment(q, k, v, grid=E.Grid(c_q=(4, 48)), out_dir=str(tmp_path / "x"))
+    assert not (tmp_path / "x").exists()  # nothing ran, nothing written
+
+
+def test_run_experiment_is_byte_deterministic(tmp_path):  # test_experiment.cpp:146-160
+    """Repeated GPU runs emit byte-identical metrics.csv and records (only
+    run_meta.json carries timestamps): every kernel on the path is deterministic."""
+    from paper_2512_14082_b200 import experiment as E
+    q, k, v = _small_inputs()
+    grid = E.Grid(strategy=(0, 2))
+    for d in ("a", "b"):
+        E.run_experiment(q, k, v, grid=grid, proxies=(0, 1), out_dir=str(tmp_path / d), seed=7)
+    a, b = tmp_path / "a", tmp_path / "b"
+    assert (a / "metrics.csv").read_bytes() == (b / "metrics.csv").read_bytes()
+    for n in ("run_0000.json", "run_0003.json"):
+        assert (a / "records" / n).read_bytes() == (b / "records" / n).read_bytes()
