@@ -405,6 +405,9 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   if ((s = make_tmap_2d_16b(&tQ, Q, uint64_t(g.B) * g.H * g.L, g.D, 64, 64, true)) != US_OK) return s;
   if ((s = make_tmap_2d_16b(&tK, K, uint64_t(g.B) * g.H_kv * g.L, g.D, 64, 64, true)) != US_OK) return s;
   if ((s = make_tmap_2d_16b(&tV, V, uint64_t(g.B) * g.H_kv * g.L, g.D, 64, 64, true)) != US_OK) return s;
+  CUtensorMap tK3, tV3;  // attention.cu: one TMA per K / V tile (all d-chunks)
+  if ((s = make_tmap_rows_chunked(&tK3, K, uint64_t(g.B) * g.H_kv * g.L, g.D, 64)) != US_OK) return s;
+  if ((s = make_tmap_rows_chunked(&tV3, V, uint64_t(g.B) * g.H_kv * g.L, g.D, 64)) != US_OK) return s;
   AttnArgs a{};
   a.B = g.B;
   a.H = g.H;
@@ -423,7 +426,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.lse = lse;
   a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
   if (attention_impl() == 2) return launch_attention2(a, tK, tV, st);
-  return launch_attention(a, tQ, tK, tV, st);
+  return launch_attention(a, tQ, tK3, tV3, st);
 }
 
 us_status sync_check(const us_params& p, void* ws, cudaStream_t st, const char* who) {

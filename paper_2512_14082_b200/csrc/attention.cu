@@ -329,10 +329,9 @@ __global__ void __launch_bounds__(384, 1)
         uint8_t* sk = smem + s * 2 * SL::kKVBytes;
         uint8_t* sv = sk + SL::kKVBytes;
         mbar_arrive_expect_tx(&bar_kvfull[s], 2 * SL::kKVBytes);
-        for (int kc = 0; kc < SL::kChunks; ++kc) {
-          tma_load_2d_hint(sk + kc * kBS * 128, &tmK, &bar_kvfull[s], kc * 64, kvrow0 + j * kBS, pol_kv);
-          tma_load_2d_hint(sv + kc * kBS * 128, &tmV, &bar_kvfull[s], kc * 64, kvrow0 + j * kBS, pol_kv);
-        }
+        // one 3-D TMA per tile: 64 rows x all d-chunks, landing as [chunk][row][128 B]
+        tma_load_3d_hint(sk, &tmK, &bar_kvfull[s], 0, kvrow0 + j * kBS, 0, pol_kv);
+        tma_load_3d_hint(sv, &tmV, &bar_kvfull[s], 0, kvrow0 + j * kBS, 0, pol_kv);
       }
     }
     __syncwarp();

@@ -79,4 +79,29 @@ inline us_status make_tmap_2d_16b(CUtensorMap* m, const void* base, uint64_t row
   return US_OK;
 }
 
+// K / V rows [rows][D] bf16 as a 3-D map (64 elements, rows, D/64 chunks) with a
+// box of (64, box_rows, D/64): ONE TMA brings a box_rows x D tile into smem as
+// [chunk][row][128 B] (SWIZZLE_128B per 128-byte line), the layout of two
+// separate 2-D chunk loads.
+inline us_status make_tmap_rows_chunked(CUtensorMap* m, const void* base, uint64_t rows, uint32_t D,
+                                        uint32_t box_rows) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable from the driver");
+    return US_ERR_CUDA;
+  }
+  cuuint64_t dims[3] = {64, rows, D / 64};
+  cuuint64_t strides[2] = {uint64_t(D) * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, D / 64};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3-D rows x chunks) failed (" + std::to_string(int(r)) + ")");
+    return US_ERR_CUDA;
+  }
+  return US_OK;
+}
+
 }  // namespace us
