@@ -468,6 +468,13 @@ def main():
         "attention": {"bound": "tensor", "flops": flops_attn,
                       "achieved_tflops": flops_attn / (stage_ms["attention"] * 1e-3) / 1e12, "peak_tflops": tf_sust},
     }
+    # proxy (+ finalize): compressed_qk (metrics.cpp:60) over the post-softmax full square; the
+    # tensor pipe issues it three times (fp16x3 hi.hi + hi.lo + lo.hi)
+    cq, ck, ch = cfg.c_q, cfg.c_k, cfg.c_h
+    qk = 2 * (L // cq) * (L // ck) * (len(heads) // ch) * d
+    stage_roofs["proxy"] = {"bound": "tensor", "flops": qk,
+                            "achieved_tflops": qk / (stage_ms["proxy"] * 1e-3) / 1e12,
+                            "issued_tflops": 3 * qk / (stage_ms["proxy"] * 1e-3) / 1e12, "peak_tflops": tf_sust}
 
     if rank != 0:
         if dist:
