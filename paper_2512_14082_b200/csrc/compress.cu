@@ -63,7 +63,7 @@ __device__ __forceinline__ double group_sum(double v, int width) {
 // STRAT: the pooling strategy, compile-time so the mean kernel (the default path)
 // carries no registers for the max / stochastic code.
 template <int STRAT>
-__global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
+__global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
   const int chunks = a.d / 8;
   const int Lc = a.L / a.c;
   const long long total = (long long)a.B * a.planes * Lc * chunks;
