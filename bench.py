@@ -472,9 +472,20 @@ def main():
     # tensor pipe issues it three times (fp16x3 hi.hi + hi.lo + lo.hi)
     cq, ck, ch = cfg.c_q, cfg.c_k, cfg.c_h
     qk = 2 * (L // cq) * (L // ck) * (len(heads) // ch) * d
+    # MUFU floor: ex2 at 16 results / clock / SM (B300_MICROARCH, measured here by
+    # tools/ex2_rate.py) at the sustained clock; the proxy exponentiates every logit of the
+    # full square (softmax_aggregation / 4 exps, metrics.cpp:62), the attention kernel 7/8 of
+    # its issued P entries (1/8 go to the FMA-pipe polynomial)
+    mufu_per_s = 16 * 148 * (clk["sm_mhz"] or 1965.0) * 1e6
+    n_exp_proxy = (L // cq) * (L // ck) * (len(heads) // ch)
     stage_roofs["proxy"] = {"bound": "tensor", "flops": qk,
                             "achieved_tflops": qk / (stage_ms["proxy"] * 1e-3) / 1e12,
-                            "issued_tflops": 3 * qk / (stage_ms["proxy"] * 1e-3) / 1e12, "peak_tflops": tf_sust}
+                            "issued_tflops": 3 * qk / (stage_ms["proxy"] * 1e-3) / 1e12, "peak_tflops": tf_sust,
+                            "mufu_floor_ms": n_exp_proxy / mufu_per_s * 1e3}
+    if tile_eff:
+        useful_exp = selected * 64 * 64
+        stage_roofs["attention"]["mufu_floor_ms"] = useful_exp * 7 / 8 / mufu_per_s * 1e3
+        stage_roofs["attention"]["tensor_floor_ms_issued"] = (issued_attn / (tf_sust * 1e12)) * 1e3
 
     if rank != 0:
         if dist:
