@@ -226,3 +226,56 @@ def test_pooling_ablations_masks_bit_exact(strategy):
     r = _run_case(4096, 4, 2, 128, 0.95, O.POST_SOFTMAX, 1, 31 + strategy, strategy=strategy)
     flips = int((r["gpu_mask"] != r["ref_mask"]).sum())
     assert flips == 0, flips
+
+
+def _fuzz_cases(n=24, seed=2026):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        H_kv = int(rng.choice([1, 2, 4]))
+        G = int(rng.choice([1, 2, 3, 4, 7]))
+        H = H_kv * G
+        if H > 12:
+            continue
+        c_h = int(rng.choice([c for c in (1, 2, 3, 4) if H % c == 0]))
+        c_q, c_k = int(rng.choice([2, 4, 8, 16])), int(rng.choice([2, 4, 8, 16]))
+        out.append(dict(L=int(rng.choice([1024, 2048, 3072])), H=H, H_kv=H_kv, d=int(rng.choice([64, 128])),
+                        c_q=c_q, c_k=c_k, c_h=c_h, P=float(rng.choice([0.8, 0.9, 0.95, 1.0])),
+                        mode=int(rng.choice([O.POST_SOFTMAX, O.PRE_SOFTMAX])),
+                        topk=int(rng.choice([0, 0, 3])), seed=int(rng.integers(1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: "L{L}_H{H}_kv{H_kv}_d{d}_c{c_q}x{c_k}x{c_h}_P{P}_m{mode}_k{topk}".format(**c))
+def test_fuzz_pipeline_against_oracle(case):
+    """Seeded random configurations across the GPU envelope (GQA groups incl. odd,
+    head compression, every S/c, post / pre softmax, Top-P and top-k): the mask is
+    the reference rule applied to the GPU's scores (exact), scores are fp32-class
+    close to the fp64 reference, flips vs the fp64 rule stay near-tie only, and the
+    output equals fp64 sparse attention on the GPU's mask within the bf16 bound."""
+    c = case
+    Q, K, V, _ = workload(O.WL_PLANTED, c["L"], c["H"], c["H_kv"], c["d"], c["seed"] % 1000, gain=8.0)
+    sm = us().SELECT_TOP_K if c["topk"] else us().SELECT_TOP_P
+    cfg = us().CompressionConfig(c_q=c["c_q"], c_k=c["c_k"], c_h=c["c_h"], P=c["P"], causal_mode=c["mode"],
+                                 select_mode=sm, top_k=c["topk"])
+    res = us().unisparse_attn(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1), cfg, with_scores=True)
+    torch.cuda.synchronize()
+    H, N = c["H"], c["L"] // 64
+    g_scores = res.report.mask.scores[0].cpu().numpy().astype(np.float64)
+    g_mask = res.report.mask.dense_mask()[0].cpu().numpy()
+    oc = O.cfg(H, c["L"], c["d"], 64, H_kv=c["H_kv"], c_q=c["c_q"], c_k=c["c_k"], c_h=c["c_h"],
+               causal_mode=c["mode"], P=c["P"])
+    Qc, Kc = O.compress(oc, Q, K)
+    r_scores = O.proxy_scores(oc, Qc, Kc)
+    sel = O.TOP_K if c["topk"] else O.TOP_P
+    mirror, _ = O.build_block_mask(g_scores, H, c["c_h"], c["P"], select_mode=sel, top_k=c["topk"])
+    assert (mirror == g_mask).all()
+    tri = np.tril(np.ones((N, N), bool))
+    big = r_scores[:, tri] > 1e-6
+    rel = np.abs(g_scores - r_scores)[:, tri][big] / r_scores[:, tri][big]
+    assert rel.max() < 1e-3, rel.max()
+    ref_mask, _ = O.build_block_mask(r_scores, H, c["c_h"], c["P"], select_mode=sel, top_k=c["topk"])
+    assert int((ref_mask != g_mask).sum()) <= max(2, H * N * (N + 1) // 2 // 20000)
+    Og = res.O.float().cpu().numpy()[0]
+    Or, _ = O.block_sparse_attention(Q, K, V, g_mask, 64)
+    assert np.abs(Og - Or).max() <= 1e-2 * np.abs(Or).max() + 1e-4
