@@ -156,6 +156,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def tile_efficiency(dm, G: int, selected: int) -> dict:
+    """Issued M=128 tile steps of attention.cu for a [H, N, N] causal mask: the CTA
+    work items of decode_item (4 query groups: 4 heads of a KV group / 2 heads x 2
+    query blocks / 1 head x 4 query blocks) and the kernel's pairing of the groups
+    into two tiles (smallest longer union, then smallest total; ties keep 01|23)."""
+    import torch
+    H, N, _ = dm.shape
+    if G % 4 == 0:
+        M = dm.view(H // 4, 4, N, N).permute(0, 2, 1, 3).reshape(-1, 4, N)
+    elif G == 2:
+        Np = (N + 1) // 2
+        pad = torch.zeros((H, 2 * Np, N), dtype=dm.dtype, device=dm.device)
+        pad[:, :N] = dm
+        x = pad.view(H // 2, 2, Np, 2, N)              # [kv, head-in-pair, pair, (ia, ib), N]
+        M = torch.stack([x[:, 0, :, 1], x[:, 1, :, 1], x[:, 0, :, 0], x[:, 1, :, 0]], 2).reshape(-1, 4, N)
+    else:
+        Nq = (N + 3) // 4
+        pad = torch.zeros((H, 4 * Nq, N), dtype=dm.dtype, device=dm.device)
+        pad[:, :N] = dm
+        M = pad.view(H, Nq, 4, N).flip(2).reshape(-1, 4, N)
+    u = lambda a, b: (M[:, a] | M[:, b]).sum(-1)
+    cand = [(u(0, 1), u(2, 3)), (u(0, 2), u(1, 3)), (u(0, 3), u(1, 2))]
+    keys = torch.stack([torch.maximum(a, b) * 4096 + a + b for a, b in cand])   # [3, items]
+    tot = torch.stack([a + b for a, b in cand])
+    best = keys.argmin(0)                                # first minimum = the kernel's strict '<'
+    issued = int(tot.gather(0, best[None]).sum().item())
+    return {"useful_group_steps": selected, "issued_tile_steps": issued,
+            "rows_useful_fraction": selected / (2.0 * issued) if issued else 1.0}
+
+
 # ----------------------------------------------------------------------------- CPU path
 _CPU_CACHE: dict = {}
 
@@ -309,13 +339,10 @@ def main():
     # tile efficiency of attn_kernel: each M=128 tile (two 64-row query groups that
     # share a KV head) issues S / P.V for the UNION of its groups' selections
     tile_eff = None
-    if G % 4 == 0 and len(heads) % 4 == 0:
-        dm = eng.sel.dense_mask()[0]                                   # [H, N, N] bool
-        pairs = dm.view(len(heads) // 2, 2, N, N)
-        union = (pairs[:, 0] | pairs[:, 1]).sum().item()
-        tile_eff = {"useful_group_steps": selected, "issued_tile_steps": int(union),
-                    "rows_useful_fraction": selected / (2.0 * union)}
-        del dm, pairs
+    try:
+        tile_eff = tile_efficiency(eng.sel.dense_mask()[0], G, selected)  # mirrors attention.cu's items
+    except Exception as e:  # noqa: BLE001 - reporting only
+        log("tile efficiency unavailable:", e)
     causal = len(heads) * N * (N + 1) // 2
     rho = 1.0 - selected / causal
 
