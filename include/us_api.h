@@ -213,7 +213,8 @@ us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, 
 
 /* Block-sparse attention kernel used by every call in this process:
  * 1 = attention.cu (two M=128 tiles per CTA, 64-key steps; default),
- * 2 = attention2.cu (one tile per CTA, 128-key steps). Both compute the same
+ * 2 = attention2.cu (one tile per CTA, 128-key steps), 3 = attention.cu with one
+ * tile (two query groups) per CTA and two CTAs per SM. All compute the same
  * function; the environment variable US_ATTN_IMPL sets the initial choice. */
 us_status us_set_attention_impl(int32_t impl);
 

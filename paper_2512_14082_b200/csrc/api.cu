@@ -379,7 +379,7 @@ int attention_impl() {
   int v = g_attn_impl.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = std::getenv("US_ATTN_IMPL");
-    v = (e && std::atoi(e) == 2) ? 2 : 1;
+    v = (e && (std::atoi(e) == 2 || std::atoi(e) == 3)) ? std::atoi(e) : 1;
     g_attn_impl.store(v, std::memory_order_relaxed);
   }
   return v;
@@ -426,6 +426,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.lse = lse;
   a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
   if (attention_impl() == 2) return launch_attention2(a, tK, tV, st);
+  a.one_tile = attention_impl() == 3 ? 1 : 0;
   return launch_attention(a, tQ, tK3, tV3, st);
 }
 
@@ -505,8 +506,8 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
 }
 
 us_status us_set_attention_impl(int32_t impl) {
-  if (impl != 1 && impl != 2) {
-    set_error("us_set_attention_impl: impl must be 1 (64-key steps) or 2 (128-key steps)");
+  if (impl != 1 && impl != 2 && impl != 3) {
+    set_error("us_set_attention_impl: impl must be 1 (two tiles per CTA), 2 (128-key steps) or 3 (one tile per CTA)");
     return US_ERR_INVALID_ARGUMENT;
   }
   g_attn_impl.store(impl, std::memory_order_relaxed);

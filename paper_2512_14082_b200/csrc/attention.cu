@@ -83,17 +83,19 @@ constexpr int kMaxW = kMaxN / 32;
 
 // K/V ring depth: a 64-key K+V tile takes ~1-2 us to land from L2, so the ring
 // must cover several steps of prefetch.
-template <int D>
-constexpr int stages_for() { return D == 128 ? 5 : 10; }
+// NT = tiles per CTA: 2 (one CTA per SM, the four groups share each K/V tile) or 1
+// (two CTAs per SM, independent: no CTA waits on a shorter partner tile).
+template <int D, int NT>
+constexpr int stages_for() { return NT == 2 ? (D == 128 ? 5 : 10) : (D == 128 ? 2 : 4); }
 
-template <int D>
+template <int D, int NT = 2>
 struct AttnSmem {
-  static constexpr int kST = stages_for<D>();
+  static constexpr int kST = stages_for<D, NT>();
   static constexpr int kChunks = D / 64;
   static constexpr int kKVBytes = kBS * D * 2;       // one of K / V per stage
   static constexpr int kRingBytes = kST * 2 * kKVBytes;
   static constexpr int kPBytes = 128 * kBS * 2;      // per tile: 128 rows x 64 keys bf16
-  static constexpr int kBytes = kRingBytes + 2 * kPBytes;
+  static constexpr int kBytes = kRingBytes + NT * kPBytes;
 };
 
 // TMEM columns of tile X start at X * 256: S [0,64), O [64, 64+D), Q [192, 192+D/2).
@@ -172,11 +174,44 @@ __device__ __forceinline__ Groups decode_item(const AttnArgs& a, int item) {
   return g;
 }
 
-template <int D>
-__global__ void __launch_bounds__(384, 1)
+// One-tile CTAs: two groups that read the same KV head — two heads of a KV group at
+// one query block (G even) or one head at query blocks (i, i-1) (G odd); groups 2, 3
+// are disabled copies of group 0.
+__device__ __forceinline__ Groups decode_pair(const AttnArgs& a, int item) {
+  Groups g;
+  const int G = a.H / a.H_kv;
+  if (G % 2 == 0) {
+    const int pairs = a.H / 2;
+    const int i = a.N - 1 - item % a.N;
+    const int bp = item / a.N;
+    g.b = bp / pairs;
+    const int h0 = (bp % pairs) * 2;
+    g.h[0] = h0;
+    g.h[1] = h0 + 1;
+    g.i[0] = g.i[1] = i;
+    g.en[0] = g.en[1] = true;
+  } else {
+    const int np = (a.N + 1) / 2;
+    const int ip = np - 1 - item % np;
+    const int bh = item / np;
+    g.b = bh / a.H;
+    g.h[0] = g.h[1] = bh % a.H;
+    g.i[0] = 2 * ip + 1;
+    g.i[1] = 2 * ip;
+    g.en[0] = g.i[0] < a.N;
+    g.en[1] = true;
+  }
+  g.h[2] = g.h[3] = g.h[1];
+  g.i[2] = g.i[3] = g.i[1];
+  g.en[2] = g.en[3] = false;
+  return g;
+}
+
+template <int D, int NT>
+__global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
     attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  using SL = AttnSmem<D>;
+  using SL = AttnSmem<D, NT>;
   constexpr int kST = SL::kST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -197,7 +232,7 @@ __global__ void __launch_bounds__(384, 1)
   const bool us_traced = blockIdx.x == g_attn_trace_cta;
 #endif
   const int G = a.H / a.H_kv;
-  const Groups gr = decode_item(a, blockIdx.x);
+  const Groups gr = NT == 2 ? decode_item(a, blockIdx.x) : decode_pair(a, blockIdx.x);
   const int kvh = gr.h[0] / G;
   int jmax = -1;
   for (int k = 0; k < 4; ++k)
@@ -213,13 +248,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int s = 0; s < kST; ++s) {
       mbar_init(&bar_kvfull[s], 1);
-      mbar_init(&bar_kvempty[s], 2);
+      mbar_init(&bar_kvempty[s], NT);
     }
     mbar_init(&bar_ofull[0], 1);
     mbar_init(&bar_ofull[1], 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
+  if (warp == 1) tmem_alloc(&tmem_base_sh, NT * 256);
   if (warp == 2) {
     // mask rows restricted to the causal prefix j <= i_g, then the ascending union list
     const int nw = jmax >= 0 ? (jmax >> 5) + 1 : 0;
@@ -261,8 +296,8 @@ __global__ void __launch_bounds__(384, 1)
     c12 = __reduce_add_sync(0xffffffffu, c12);
     int pr = 0, best = max(c01, c23) * 4096 + c01 + c23;
     const int k1 = max(c02, c13) * 4096 + c02 + c13, k2 = max(c03, c12) * 4096 + c03 + c12;
-    if (a.pairing && k1 < best) { pr = 1; best = k1; }
-    if (a.pairing && k2 < best) { pr = 2; best = k2; }
+    if (NT == 2 && a.pairing && k1 < best) { pr = 1; best = k1; }
+    if (NT == 2 && a.pairing && k2 < best) { pr = 2; best = k2; }
     // slot s (tile s / 2, rows (s & 1) * 64 ..) holds group perm[s]
     const uint32_t perm = pr == 0 ? 0xE4u : pr == 1 ? 0xD8u : 0x9Cu;  // 2-bit fields: 0123 / 0213 / 0312
     int base = 0;
@@ -335,7 +370,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1 || warp == 3) {
+  } else if (warp == 1 || (NT == 2 && warp == 3)) {
     // ------------------------------------------------------------ MMA issuers
     const int x = warp == 1 ? 0 : 1;
     constexpr uint32_t idesc_s = idesc_f16(128, kBS, /*bf16*/ 1, false, false);
@@ -410,9 +445,9 @@ __global__ void __launch_bounds__(384, 1)
     }
     if (elect_one()) umma_commit(&bar_ofull[x]);
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp >= (NT == 2 ? 4 : 2)) {
     // ------------------------------------------------------------ softmax / epilogue
-    const int x = (warp - 4) >> 2;  // tile
+    const int x = NT == 2 ? (warp - 4) >> 2 : 0;  // tile
     const int q = warp & 3;         // TMEM lane quarter
     const int row = q * 32 + lane;
     const int slot = 2 * x + (row >> 6), rloc = row & 63;
@@ -601,24 +636,31 @@ __global__ void __launch_bounds__(384, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == 1) tmem_dealloc(tmem, NT * 256);
 }
 
-template <int D>
+template <int D, int NT>
 us_status launch_attn_t(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                         const CUtensorMap& tmV, cudaStream_t st) {
-  const int smem = AttnSmem<D>::kBytes + 1024;  // + alignment slack
+  const int smem = AttnSmem<D, NT>::kBytes + 1024;  // + alignment slack
   static bool attr_set = false;
   if (!attr_set) {
-    US_CUDA_TRY(cudaFuncSetAttribute(attn_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+    US_CUDA_TRY(cudaFuncSetAttribute(attn_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                 "attn_kernel smem attribute");
     attr_set = true;
   }
   long long items;
-  if (a.group_mode == 0) items = (long long)a.B * (a.H / 4) * a.N;
-  else if (a.group_mode == 1) items = (long long)a.B * a.H_kv * ((a.N + 1) / 2);
-  else items = (long long)a.B * a.H * ((a.N + 3) / 4);
-  attn_kernel<D><<<unsigned(items), 384, smem, st>>>(tmQ, tmK, tmV, a);
+  if (NT == 1) {
+    const int G = a.H / a.H_kv;
+    items = G % 2 == 0 ? (long long)a.B * (a.H / 2) * a.N : (long long)a.B * a.H * ((a.N + 1) / 2);
+  } else if (a.group_mode == 0) {
+    items = (long long)a.B * (a.H / 4) * a.N;
+  } else if (a.group_mode == 1) {
+    items = (long long)a.B * a.H_kv * ((a.N + 1) / 2);
+  } else {
+    items = (long long)a.B * a.H * ((a.N + 3) / 4);
+  }
+  attn_kernel<D, NT><<<unsigned(items), NT == 2 ? 384 : 192, smem, st>>>(tmQ, tmK, tmV, a);
   US_LAUNCH_CHECK("attn_kernel");
   return US_OK;
 }
@@ -631,8 +673,13 @@ us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUte
     set_error("attention: N (=L/S) above 4096 is not supported on the GPU path");
     return US_ERR_UNSUPPORTED;
   }
-  if (a.D == 128) return launch_attn_t<128>(a, tmQ, tmK, tmV, st);
-  if (a.D == 64) return launch_attn_t<64>(a, tmQ, tmK, tmV, st);
+  if (a.one_tile) {
+    if (a.D == 128) return launch_attn_t<128, 1>(a, tmQ, tmK, tmV, st);
+    if (a.D == 64) return launch_attn_t<64, 1>(a, tmQ, tmK, tmV, st);
+  } else {
+    if (a.D == 128) return launch_attn_t<128, 2>(a, tmQ, tmK, tmV, st);
+    if (a.D == 64) return launch_attn_t<64, 2>(a, tmQ, tmK, tmV, st);
+  }
   set_error("attention: d_k must be 64 or 128 on the GPU path");
   return US_ERR_UNSUPPORTED;
 }

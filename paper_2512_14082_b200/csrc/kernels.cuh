@@ -121,6 +121,7 @@ struct AttnArgs {
   float* lse;           // [B][H][L] (nullable)
   float scale_log2;
   int pairing;          // 1: pair the CTA's groups into tiles by union size (0: fixed 01|23)
+  int one_tile;         // 1: one M=128 tile (two groups) per CTA, two CTAs per SM
 };
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);

@@ -280,7 +280,7 @@ def test_attention_impls_agree(H, H_kv, d):
     lib = us().api.lib()
     lib.us_set_attention_impl.argtypes = [ctypes.c_int32]
     try:
-        for impl in (2, 1):
+        for impl in (3, 2, 1):
             assert lib.us_set_attention_impl(impl) == 0
             Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
             Og = Og.float().cpu().numpy()
