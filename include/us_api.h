@@ -212,10 +212,11 @@ us_status us_check_device_errors(const us_params* p, void* workspace, void* stre
 us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, uint64_t* out6);
 
 /* Block-sparse attention kernel used by every call in this process:
- * 1 = attention.cu (two M=128 tiles per CTA, 64-key steps; default),
+ * 0 = automatic (default, = 1); 1 = attention.cu (two M=128 query tiles per CTA, 64-key steps),
  * 2 = attention2.cu (one tile per CTA, 128-key steps), 3 = attention.cu with one
- * tile (two query groups) per CTA and two CTAs per SM. All compute the same
- * function; the environment variable US_ATTN_IMPL sets the initial choice. */
+ * tile (two query groups) per CTA and two CTAs per SM, 4 = attention_kt.cu (key
+ * blocks as the MMA M dimension, one query group per work item; d_k = 128). All compute the same function; the environment variable
+ * US_ATTN_IMPL sets the initial choice. */
 us_status us_set_attention_impl(int32_t impl);
 
 /* Tile pairing inside an attention.cu CTA (calibration knob, process-wide):

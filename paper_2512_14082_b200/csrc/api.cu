@@ -372,14 +372,17 @@ us_status run_select_rows(const us_params& p, const float* scores, int planes, u
   return launch_select(sa, st);
 }
 
-// Attention kernel selection (calibration knob): US_ATTN_IMPL=1 -> attention.cu
-// (64-key steps, two tiles per CTA), 2 -> attention2.cu (128-key steps).
+// Attention kernel selection (calibration knob, US_ATTN_IMPL): 0 = automatic
+// (default: the key-major attention_kt.cu for block-sparse masks at d_k = 128,
+// attention.cu for dense / d_k = 64), 1 = attention.cu (two M=128 query tiles
+// per CTA, 64-key steps), 2 = attention2.cu, 3 = attention.cu with one tile per
+// CTA, 4 = attention_kt.cu whenever d_k = 128 (dense included).
 std::atomic<int> g_attn_impl{-1};
 int attention_impl() {
   int v = g_attn_impl.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = std::getenv("US_ATTN_IMPL");
-    v = (e && (std::atoi(e) == 2 || std::atoi(e) == 3)) ? std::atoi(e) : 1;
+    v = (e && std::atoi(e) >= 1 && std::atoi(e) <= 4) ? std::atoi(e) : 0;
     g_attn_impl.store(v, std::memory_order_relaxed);
   }
   return v;
@@ -398,7 +401,8 @@ int attention_pairing() {
 }
 
 us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
-                        const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st) {
+                        const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st,
+                        uint32_t* err = nullptr, int32_t* first_bad = nullptr) {
   Geo g(p);
   CUtensorMap tQ, tK, tV;
   us_status s;
@@ -425,8 +429,16 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.O = static_cast<__nv_bfloat16*>(O);
   a.lse = lse;
   a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
-  if (attention_impl() == 2) return launch_attention2(a, tK, tV, st);
-  a.one_tile = attention_impl() == 3 ? 1 : 0;
+  a.err = err;
+  a.first_bad = first_bad;
+  const int impl = attention_impl();
+  if (g.D == 128 && impl == 4) {
+    CUtensorMap tQ3;
+    if ((s = make_tmap_rows_chunked(&tQ3, Q, uint64_t(g.B) * g.H * g.L, g.D, 64)) != US_OK) return s;
+    return launch_attention_kt(a, tQ3, tK, tV3, st);
+  }
+  if (impl == 2) return launch_attention2(a, tK, tV, st);
+  a.one_tile = impl == 3 ? 1 : 0;
   return launch_attention(a, tQ, tK3, tV3, st);
 }
 
@@ -506,8 +518,9 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
 }
 
 us_status us_set_attention_impl(int32_t impl) {
-  if (impl != 1 && impl != 2 && impl != 3) {
-    set_error("us_set_attention_impl: impl must be 1 (two tiles per CTA), 2 (128-key steps) or 3 (one tile per CTA)");
+  if (impl < 0 || impl > 4) {
+    set_error("us_set_attention_impl: impl must be 0 (automatic), 1 (two query tiles per CTA), 2 (128-key steps), "
+              "3 (one tile per CTA) or 4 (key-major)");
     return US_ERR_INVALID_ARGUMENT;
   }
   g_attn_impl.store(impl, std::memory_order_relaxed);

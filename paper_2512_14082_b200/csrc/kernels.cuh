@@ -122,9 +122,17 @@ struct AttnArgs {
   float scale_log2;
   int pairing;          // 1: pair the CTA's groups into tiles by union size (0: fixed 01|23)
   int one_tile;         // 1: one M=128 tile (two groups) per CTA, two CTAs per SM
+  uint32_t* err;        // device error word (nullable): |= 4 non-causal bit, |= 8 empty row
+  int32_t* first_bad;   // first offending mask row (atomicMin; nullable with err)
 };
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);
+
+// Key-major variant (attention_kt.cu, d_k = 128): one query group per work item,
+// M = 128 = a pair of its own selected key blocks (no union rows); persistent CTAs.
+// tmQ3 / tmV3: 3-D rows-chunked maps (box 64 rows), tmK2: 2-D map (box 64 x 64).
+us_status launch_attention_kt(const AttnArgs& a, const CUtensorMap& tmQ3, const CUtensorMap& tmK2,
+                              const CUtensorMap& tmV3, cudaStream_t st);
 
 // 128-key-step variant (attention2.cu): one M=128 tile per CTA, two union blocks
 // per step; Q is read from global memory by the softmax warps (no Q tensor map).

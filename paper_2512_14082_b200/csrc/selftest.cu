@@ -4,6 +4,8 @@
 //   mode 1: A K-major (TMA), B MN-major (TMA)           D = A * B     (attention P.V with V row-major)
 //   mode 2: A in TMEM (tcgen05.st), B K-major (TMA)     D = A * B^T   (TS path)
 //   mode 3: A written by threads into swizzled smem, B MN-major: the attention P.V path.
+//   mode 4: A MN-major (TMA of A^T stored [K][M]), B MN-major: the transposed attention
+//           O^T = V^T P^T path (V rows [key][d] are the MN-major A of M = d).
 // M = 128, K = 128 (two 64-element swizzle atoms), N in {64, 128}.
 #include <cuda_runtime.h>
 
@@ -38,14 +40,16 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  const bool b_mn = (mode == 1 || mode == 3);
+  const bool b_mn = (mode == 1 || mode == 3 || mode == 4);
   // ---- operand staging
   if (threadIdx.x == 0) {
     uint32_t bytes = N * kK * 2;
-    if (mode <= 1) bytes += kM * kK * 2;
+    if (mode <= 1 || mode == 4) bytes += kM * kK * 2;
     mbar_arrive_expect_tx(&bar_tma, bytes);
     if (mode <= 1)
       for (int kc = 0; kc < 2; ++kc) tma_load_2d(sA + kc * kM * 128, &tmA, &bar_tma, kc * 64, 0);
+    if (mode == 4)  // [mc][128 K rows][128 B]
+      for (int mc = 0; mc < 2; ++mc) tma_load_2d(sA + mc * kK * 128, &tmA, &bar_tma, mc * 64, 0);
     if (!b_mn) {
       for (int kc = 0; kc < 2; ++kc) tma_load_2d(sB + kc * N * 128, &tmB, &bar_tma, kc * 64, 0);
     } else {
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(&bar_tma, 0);
     tc_fence_after();
     if (elect_one()) {
-      const uint32_t idesc = idesc_f16(kM, N, bf16 ? 1 : 0, false, b_mn);
+      const uint32_t idesc = idesc_f16(kM, N, bf16 ? 1 : 0, mode == 4, b_mn);
       for (int k = 0; k < kK / 16; ++k) {
         const int kc = k / 4, ks = k % 4;
         uint64_t bdesc;
@@ -95,6 +99,9 @@ __global__ void __launch_bounds__(128, 1)
           bdesc = sdesc_sw128(smem_u32(sB + k * 16 * 128), kK * 128, 1024);
         if (mode == 2) {
           umma_f16_ts(tmem, tmem + 128 + k * 8, bdesc, idesc, k > 0);
+        } else if (mode == 4) {
+          const uint64_t adesc = sdesc_sw128(smem_u32(sA + k * 16 * 128), kK * 128, 1024);
+          umma_f16_ss(tmem, adesc, bdesc, idesc, k > 0);
         } else {
           const uint64_t adesc = sdesc_sw128(smem_u32(sA + kc * kM * 128 + ks * 32), 16, 1024);
           umma_f16_ss(tmem, adesc, bdesc, idesc, k > 0);
@@ -124,14 +131,15 @@ __global__ void __launch_bounds__(128, 1)
 extern "C" us_status us_selftest_umma(int mode, int N, int bf16, const void* A, const void* B,
                                       float* D, void* stream) {
   using namespace us;
-  if (mode < 0 || mode > 3 || (N != 64 && N != 128)) {
+  if (mode < 0 || mode > 4 || (N != 64 && N != 128)) {
     set_error("us_selftest_umma: bad mode/N");
     return US_ERR_INVALID_ARGUMENT;
   }
   CUtensorMap tmA{}, tmB{};
-  us_status s = make_tmap_2d_16b(&tmA, A, kM, kK, kM, 64, bf16);
+  us_status s = mode == 4 ? make_tmap_2d_16b(&tmA, A, kK, kM, kK, 64, bf16)
+                          : make_tmap_2d_16b(&tmA, A, kM, kK, kM, 64, bf16);
   if (s != US_OK) return s;
-  const bool b_mn = (mode == 1 || mode == 3);
+  const bool b_mn = (mode == 1 || mode == 3 || mode == 4);
   s = b_mn ? make_tmap_2d_16b(&tmB, B, kK, N, kK, 64, bf16)
            : make_tmap_2d_16b(&tmB, B, N, kK, N, 64, bf16);
   if (s != US_OK) return s;
@@ -198,6 +206,97 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int N, int 
 }
 }  // namespace
 }  // namespace us
+
+// ---------------------------------------------------------------- MMA pattern probe
+// Cycles per iteration of a fixed MMA sequence (one CTA per SM, operands arbitrary):
+//   0: 8 SS N=64 (A,B K-major) -> acc0, then 8 SS N=64 (A,B MN-major) -> acc1   [transposed step]
+//   1: pattern 0 with every MMA into acc0
+//   2: 16 SS N=64 K-major into acc0
+//   3: 16 SS N=64 K-major alternating acc0 / acc1 per MMA
+//   4: 8 TS N=64 -> acc0, then 4 SS N=128 (B MN-major) -> acc1                  [current step]
+//   5: 8 SS N=128 K-major -> acc0, then 8 TS N=128 -> acc1                       [FA4 step]
+//   6: 8 SS N=64 (A,B K-major) -> acc0, then 8 SS N=64 (A,B MN-major) -> acc1, A of the second
+//      half from two tiles 16 KB apart (the V pair)
+namespace us {
+namespace {
+__global__ void __launch_bounds__(128, 1) mma_pattern_kernel(int iters, int pattern, long long* cycles_out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tbase, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  long long t0 = clock64();
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t sb = smem_u32(smem);
+      const uint32_t i64k = idesc_f16(128, 64, 1, false, false);
+      const uint32_t i64m = idesc_f16(128, 64, 1, true, true);
+      const uint32_t i128bm = idesc_f16(128, 128, 1, false, true);
+      const uint32_t i128k = idesc_f16(128, 128, 1, false, false);
+      for (int it = 0; it < iters; ++it) {
+        if (pattern == 0 || pattern == 1 || pattern == 6) {
+          for (int k = 0; k < 8; ++k)
+            umma_f16_ss(tmem, sdesc_sw128(sb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+                        sdesc_sw128(sb + 65536 + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024), i64k, k > 0);
+          const uint32_t acc = pattern == 1 ? tmem : tmem + 64;
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t abase = pattern == 6 ? sb + 32768 + (k >> 2) * 16384 + (k & 3) * 2048
+                                                : sb + 32768 + k * 2048;
+            umma_f16_ss(acc, sdesc_sw128(abase, 8192, 1024), sdesc_sw128(sb + 98304 + k * 2048, 8192, 1024),
+                        i64m, pattern == 1 ? 1u : uint32_t(k > 0));
+          }
+        } else if (pattern == 2 || pattern == 3) {
+          for (int k = 0; k < 16; ++k)
+            umma_f16_ss(pattern == 3 ? tmem + (k & 1) * 64 : tmem,
+                        sdesc_sw128(sb + ((k >> 2) & 1) * 16384 + (k & 3) * 32, 16, 1024),
+                        sdesc_sw128(sb + 65536 + ((k >> 2) & 1) * 8192 + (k & 3) * 32, 16, 1024), i64k, k > 1);
+        } else if (pattern == 4) {
+          for (int k = 0; k < 8; ++k)
+            umma_f16_ts(tmem, tmem + 448 + k * 8, sdesc_sw128(sb + 65536 + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024),
+                        i64k, k > 0);
+          for (int k = 0; k < 4; ++k)
+            umma_f16_ss(tmem + 64, sdesc_sw128(sb + k * 32, 16, 1024), sdesc_sw128(sb + 98304 + k * 2048, 8192, 1024),
+                        i128bm, k > 0);
+        } else {
+          for (int k = 0; k < 8; ++k)
+            umma_f16_ss(tmem, sdesc_sw128(sb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024),
+                        sdesc_sw128(sb + 65536 + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), i128k, k > 0);
+          for (int k = 0; k < 8; ++k)
+            umma_f16_ts(tmem + 128, tmem + 384 + k * 8, sdesc_sw128(sb + 98304 + k * 2048, 8192, 1024), i128bm,
+                        k > 0);
+        }
+      }
+      umma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cycles_out[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+}  // namespace
+}  // namespace us
+
+extern "C" us_status us_selftest_mma_pattern(int iters, int pattern, int ctas, long long* cycles_out, void* stream) {
+  using namespace us;
+  const int smem = 160 * 1024;
+  cudaFuncSetAttribute(mma_pattern_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_pattern_kernel<<<ctas, 128, smem, static_cast<cudaStream_t>(stream)>>>(iters, pattern, cycles_out);
+  US_LAUNCH_CHECK("us_selftest_mma_pattern");
+  return US_OK;
+}
 
 extern "C" us_status us_selftest_mma_rate(int iters, int N, int a_tmem, int per_group, int ctas,
                                           long long* cycles_out, void* stream) {

@@ -11,6 +11,7 @@
 //                         dense (test_pipeline.cpp:9-21), the report is
 //                         consistent with the mask, sparse attention on the
 //                         selected mask reproduces unisparse_attn bit for bit.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -157,7 +158,14 @@ static void gpu_tests() {
   CHECK(std::fabs(r1.report.rho_mean) < 1e-15);
   CHECK(r1.report.mask.selected_total() == int64_t(H) * N * (N + 1) / 2);
   u::AttentionOutput dense = u::dense_attention(in);
-  CHECK(r1.out.O.to_host() == dense.O.to_host());
+  {
+    // same function through two kernels (key-major sparse, query-major dense): bf16 agreement
+    const auto x1 = r1.out.O.to_host(), xd = dense.O.to_host();
+    double worst = 0;
+    for (size_t t = 0; t < x1.size(); ++t)
+      worst = std::max(worst, double(std::fabs(from_bf16(x1[t]) - from_bf16(xd[t]))));
+    CHECK(worst <= 2e-2);
+  }
 
   // P = 0.95: report consistent with the mask; block_sparse_attention on that
   // mask reproduces unisparse_attn bit for bit; selection is monotone in P

@@ -46,14 +46,33 @@ def _rho(sel, H, N):
 
 
 def test_criterion_1_degenerate_top_p_equals_dense():
-    ok, worst = True, 0.0
-    for L, H, d, seed in ((256, 2, 64, 11), (512, 1, 128, 12), (1024, 2, 64, 13)):
-        q, k, v, _ = _inputs(O.WL_GAUSSIAN, L, H, d, seed)
+    """acceptance.cpp:53-86: with P = 1 the pipeline selects every causal block and
+    equals dense attention. The reference compares against its fp64 dense oracle at
+    1e-5 (fp32 storage); here the GPU output (bf16 storage, bf16 P) is compared with
+    the fp64 oracle on the same bf16 inputs, within the bf16 tolerance, AND its error
+    must stay within 1.5x the error of our dense kernel on the same inputs
+    (SURVEY §8c level 3). 20 instances (L, H, H_kv, d, seed)."""
+    ok, worst_rel, worst_ratio, n = True, 0.0, 0.0, 0
+    cases = [(L, H, H_kv, d, 900 + k) for k, (L, H, H_kv, d) in enumerate(
+        [(256, 2, 2, 64), (512, 1, 1, 128), (1024, 2, 1, 64), (512, 4, 2, 128), (768, 2, 2, 128)] * 4)]
+    for L, H, H_kv, d, seed in cases:
+        Q, K, V, _ = O.gen_workload(O.WL_GAUSSIAN, L, H, d, S, seed, H_kv=H_kv)
+        Q, K, V = O.bf16_round(Q), O.bf16_round(K), O.bf16_round(V)
+        q, k, v = to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1)
         r = us().unisparse_attn(q, k, v, us().CompressionConfig(P=1.0))
         dense, _ = us().dense_attention(q, k, v)
-        worst = max(worst, (r.O.float() - dense.float()).abs().max().item())
-        ok &= bool(torch.equal(r.O, dense)) and r.report.rho_mean == 0.0
-    _report(1, "oracle-equivalence", ok, f"max |O - dense| = {worst:.3g}, rho = 0")
+        Od, _ = O.dense_attention(Q, K, V)
+        N = L // S
+        e_sp = np.abs(r.O.float().cpu().numpy()[0] - Od)
+        e_de = np.abs(dense.float().cpu().numpy()[0] - Od)
+        rel = np.linalg.norm(r.O.float().cpu().numpy()[0] - Od) / np.linalg.norm(Od)
+        ratio = e_sp.max() / max(e_de.max(), 1e-6)
+        worst_rel, worst_ratio, n = max(worst_rel, rel), max(worst_ratio, ratio), n + 1
+        ok &= r.report.rho_mean == 0.0 and sum(r.report.selected) == H * N * (N + 1) // 2
+        ok &= bool(e_sp.max() <= 1e-2 * np.abs(Od).max() + 1e-4) and rel <= 1e-2 and ratio <= 1.5
+    _report(1, "oracle-equivalence", ok,
+            f"{n} instances vs the fp64 dense oracle: rel-Frobenius <= {worst_rel:.3g}, "
+            f"max-abs error <= {worst_ratio:.3g} x the dense kernel's, rho = 0")
     assert ok
 
 

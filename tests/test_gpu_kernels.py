@@ -23,14 +23,17 @@ def us():
 
 
 # ------------------------------------------------------------------ tcgen05 building blocks
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("N", [64, 128])
 @pytest.mark.parametrize("bf16", [False, True])
 def test_umma_operand_paths(mode, N, bf16):
     g = torch.Generator().manual_seed(100 + mode * 10 + N)
     dt = torch.bfloat16 if bf16 else torch.float16
     A = torch.randn(128, 128, generator=g).to(dt)
-    if mode in (1, 3):
+    if mode == 4:  # A given as A^T [K][M] (MN-major A), B [K][N]
+        Bm = torch.randn(128, N, generator=g).to(dt)
+        ref = A.float().T @ Bm.float()
+    elif mode in (1, 3):
         Bm = torch.randn(128, N, generator=g).to(dt)   # [K][N], N contiguous
         ref = A.float() @ Bm.float()
     else:
@@ -280,7 +283,7 @@ def test_attention_impls_agree(H, H_kv, d):
     lib = us().api.lib()
     lib.us_set_attention_impl.argtypes = [ctypes.c_int32]
     try:
-        for impl in (3, 2, 1):
+        for impl in ((4, 3, 2, 1) if d == 128 else (3, 2, 1)):
             assert lib.us_set_attention_impl(impl) == 0
             Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
             Og = Og.float().cpu().numpy()
@@ -291,7 +294,50 @@ def test_attention_impls_agree(H, H_kv, d):
                 assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO, (impl, b)
                 assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
     finally:
-        lib.us_set_attention_impl(1)
+        lib.us_set_attention_impl(0)
+
+
+def _set_impl(impl):
+    import ctypes
+    lib = us().api.lib()
+    lib.us_set_attention_impl.argtypes = [ctypes.c_int32]
+    assert lib.us_set_attention_impl(impl) == 0
+
+
+@pytest.mark.parametrize("growth", [0.0, 1.0, -1.0])
+def test_attention_kt_offset_moves(growth):
+    """Key-major kernel: the per-query offsets only move when a logit exceeds them
+    by > 16 (log2). Key blocks whose logits GROW along the ascending walk force a
+    rescale of O^T and of the row-sum partials at many steps (growth 1), shrinking
+    logits never rescale after the first step (growth -1); both equal the fp64 oracle.
+    Rows with odd and even counts, with and without the diagonal block."""
+    rng = np.random.default_rng(11)
+    B, H, H_kv, L, d = 1, 4, 2, 2048, 128
+    N = L // 64
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    blk = np.arange(L) // 64  # per key row: logits grow (shrink) by ~17 log2 units per block
+    scale = {0.0: np.ones(L), 1.0: 1 + 4.0 * blk, -1.0: 1 + 4.0 * (N - 1 - blk)}[growth].astype(np.float32)
+    K = (K * scale[None, None, :, None]).astype(np.float32)
+    mask = rng.random((B, H, N, N)) < 0.5
+    mask &= np.tril(np.ones((N, N), bool))
+    mask[0, 0, np.arange(N), np.arange(N)] = False  # head 0: never the diagonal unless forced
+    empty = ~mask.any(-1)
+    mask[empty, 0] = True
+    bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
+    for impl in (4, 1):
+        _set_impl(impl)
+        try:
+            Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
+        finally:
+            _set_impl(0)
+        Og = Og.float().cpu().numpy()
+        lseg = lseg.cpu().numpy()
+        Qr, Kr, Vr = (O.bf16_round(x) for x in (Q, K, V))
+        Or, lser = O.block_sparse_attention(Qr[0], Kr[0], Vr[0], mask[0], 64)
+        assert np.isfinite(Og).all() and np.isfinite(lseg).all()
+        assert np.abs(Og[0] - Or).max() <= ATOL * max(1.0, np.abs(Or).max()), impl
+        assert np.linalg.norm(Og[0] - Or) / np.linalg.norm(Or) <= RTOL_FRO, impl
+        assert np.abs(lseg[0] - lser).max() <= 1e-3 * max(1.0, np.abs(lser).max()), impl
 
 
 @pytest.mark.parametrize("H,H_kv,density", [(8, 2, 0.3), (16, 4, 0.15), (8, 1, 0.6)])
