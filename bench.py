@@ -244,6 +244,95 @@ def cpu_sample(cfg_name, gain, P, seconds_target=12.0, nthreads=0, seed=2512):
                                      "t_gen_s": t_gen, "mean_selected_per_row": n_sel / done_rows}
 
 
+# ----------------------------------------------------------------------------- parity sample
+def parity_sample(Q, K, V, eng, mode, sel, P, rows_per_head=4, max_heads=8, seed=2512):
+    """Parity record of the MEASURED configuration: for one Q head of
+    each KV group of this rank's shard (up to `max_heads`) and a stratified sample of
+    query blocks (always including the last, longest row), the oracle recomputes the
+    proxy row (full-row LSE over every composite key), applies the reference Top-P /
+    top-k rule, and recomputes block-sparse attention over the GPU's selection for
+    that row, from the same bf16 inputs copied back from the device. Masks must be
+    identical (each flipped block is listed with its decision margins); outputs are
+    compared by max-abs and relative Frobenius error. Test infrastructure only."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_py as O
+    from gpu_util import mask_margins
+    t0 = time.perf_counter()
+    _, H, L, d = Q.shape
+    H_kv = K.shape[1]
+    G = H // H_kv
+    S, N = 64, L // 64
+    rng = np.random.default_rng(seed)
+    kv_sample = np.linspace(0, H_kv - 1, min(H_kv, max_heads)).round().astype(int)
+    flips, decisions, nrows = [], 0, 0
+    err_max, ref_max, err2, ref2 = 0.0, 0.0, 0.0, 0.0
+    heads_done = []
+    bits = eng.sel.dense_mask()[0]  # [H, N, N] on the device
+    for kv in kv_sample:
+        h = int(kv * G + rng.integers(0, G))
+        q = Q[0, h:h + 1].float().cpu().numpy()
+        k = K[0, kv:kv + 1].float().cpu().numpy()
+        v = V[0, kv:kv + 1].float().cpu().numpy()
+        c = O.cfg(1, L, d, S, H_kv=1, P=P if mode == "top_p" else 0.95,
+                  select_mode=O.TOP_P if mode == "top_p" else O.TOP_K, top_k=0 if mode == "top_p" else int(sel))
+        Qc, Kc = O.compress(c, q, k)
+        strata = np.linspace(0, N, rows_per_head).astype(int)
+        rows = np.unique(np.concatenate([[N - 1], [rng.integers(strata[t], max(strata[t] + 1, strata[t + 1]))
+                                                   for t in range(rows_per_head - 1)]])).astype(np.int32)
+        scores = O.proxy_score_rows(c, Qc, Kc, 0, rows)
+        gmask = bits[h, rows.astype(np.int64)].cpu().numpy()  # [rows, N]
+        mask1 = np.zeros((1, N, N), np.uint8)
+        for r, i in enumerate(rows):
+            idx, _ = (O.top_p_row(scores[r, : i + 1], P) if mode == "top_p" else O.top_k_row(scores[r, : i + 1], int(sel)))
+            ref = np.zeros(N, bool)
+            ref[idx] = True
+            decisions += int(i) + 1
+            for j in np.nonzero(ref != gmask[r])[0]:
+                flips.append(dict(head=h, **mask_margins(scores[r], P if mode == "top_p" else 1.0, int(i), int(j))))
+            mask1[0, i] = gmask[r]
+        Or, _ = O.block_sparse_attention_rows(q, k, v, mask1, S, np.zeros(len(rows), np.int32), rows)
+        for r, i in enumerate(rows):
+            got = eng.O[0, h, i * S:(i + 1) * S].float().cpu().numpy()
+            e = got - Or[r]
+            err_max = max(err_max, float(np.abs(e).max()))
+            ref_max = max(ref_max, float(np.abs(Or[r]).max()))
+            err2 += float((e.astype(np.float64) ** 2).sum())
+            ref2 += float((Or[r].astype(np.float64) ** 2).sum())
+        nrows += len(rows)
+        heads_done.append(h)
+    return {"rows": nrows, "heads": heads_done, "decisions": decisions, "mask_flips": len(flips), "flips": flips[:20],
+            "max_abs_err": err_max, "max_abs_ref": ref_max, "rel_fro_err": math.sqrt(err2 / max(ref2, 1e-300)),
+            "tolerance": "masks identical; max_abs <= 1e-2*max|O_ref| + 1e-4, rel-Frobenius <= 1e-2",
+            "ok": len(flips) == 0 and err_max <= 1e-2 * ref_max + 1e-4 and math.sqrt(err2 / max(ref2, 1e-300)) <= 1e-2,
+            "oracle": "oracle/ (fp64 restatement of proxy.cpp:10-72, selection.cpp:11-48, attention.cpp:89-137)",
+            "s": time.perf_counter() - t0}
+
+
+# ----------------------------------------------------------------------------- launcher
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _self_launch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1 and forward their output. N ranks need N
+    GPUs with NCCL; with --dist-backend gloo the ranks may share one GPU (a
+    functional check of the multi-rank path, never a scaling number)."""
+    import torch
+    gloo = "gloo" in " ".join(sys.argv)
+    if not gloo and torch.cuda.device_count() < n:
+        log(f"bench.py: --gpus {n} needs {n} GPUs (found {torch.cuda.device_count()}); "
+            "use --dist-backend gloo for a functional multi-rank check on fewer GPUs")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -257,26 +346,34 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense baselines")
     ap.add_argument("--seed", type=int, default=2512)
-    ap.add_argument("--flashinfer", action="store_true", help="also time flashinfer dense prefill")
+    ap.add_argument("--no-flashinfer", action="store_true", help="skip the flashinfer dense prefill baseline")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (nccl; gloo for checks)")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="KV-head chunks of the pipelined host-buffer path")
+    ap.add_argument("--batch", type=int, default=1, help="batch items per layer (partitioned with the heads)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity sample")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch through torchrun (rank 0 prints the JSON line)
+        sys.exit(_self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     desc, H, H_kv, L, d, mode, sel = CONFIGS[args.config]
     gain = args.gain if args.gain is not None else DEFAULT_GAIN[args.config]
     P = args.P if args.P is not None else (sel if mode == "top_p" else 0.95)
     metric = "attention prefill ms/layer @128K; speedup vs dense FA; HBM/TC roofline %"
-    base = {"metric": metric, "unit": "ms/layer", "n_gpus": args.gpus, "steps": args.steps,
+    base = {"metric": metric, "unit": "ms/layer", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": f"synthetic planted_blocks (reference workloads.cpp semantics, gain={gain}, m=2, sigma=0.1), bf16"}
     config = {"workload": desc, "config": args.config, "heads": H, "kv_heads": H_kv, "seq_len": L,
               "head_dim": d, "block": 64, "c_q": 8, "c_k": 8, "c_h": 1,
               "selection": f"top_p P={P}" if mode == "top_p" else f"top_k k={sel}",
-              "causal_mode": "post-softmax-block-causal", "batch": 1,
-              "parallelism": f"head-partitioned x{world} (paper_2512_14082_b200/shard.py; no hot-path collective)",
+              "causal_mode": "post-softmax-block-causal", "batch": args.batch,
+              "parallelism": f"(batch x KV-head)-partitioned x{world} (paper_2512_14082_b200/shard.py "
+                             f"shard_layer; no hot-path collective)",
               "l2": "inputs (>=192 MB per rank) exceed the 126 MB L2; no flush needed"}
 
     if args.impl == "reference":
@@ -306,16 +403,17 @@ def main():
         dist.init_process_group(args.dist_backend, init_method="env://")
     # (modulo: lets a functional multi-rank check share one GPU; one GPU per rank in production)
     torch.cuda.set_device(local % torch.cuda.device_count())
-    from paper_2512_14082_b200.shard import gather_heads, imbalance, shard_heads
-    shards = shard_heads(H, H_kv, world)
+    from paper_2512_14082_b200.shard import gather_layer, imbalance, shard_layer
+    shards = shard_layer(args.batch, H, H_kv, world)
     shard = shards[rank]
     G = H // H_kv
     heads = list(shard.q_heads)
-    Q, K, V = workloads.planted_blocks(L, H, H_kv, d, 64, seed=args.seed, gain=gain, heads=heads)
+    Q, K, V = workloads.planted_blocks(L, H, H_kv, d, 64, seed=args.seed, gain=gain, heads=heads, B=args.batch,
+                                       batches=list(shard.batch))
     torch.cuda.synchronize()
     cfg = us.CompressionConfig(P=P) if mode == "top_p" else us.CompressionConfig(
         select_mode=us.SELECT_TOP_K, top_k=int(sel))
-    eng = us.Engine(Q, K, V, cfg)
+    eng = us.Engine(Q, K, V, cfg, head0=shard.q_heads.start)
 
     def barrier():
         if dist:
@@ -340,10 +438,16 @@ def main():
     # share a KV head) issues S / P.V for the UNION of its groups' selections
     tile_eff = None
     try:
-        tile_eff = tile_efficiency(eng.sel.dense_mask()[0], G, selected)  # mirrors attention.cu's items
+        dm = eng.sel.dense_mask()
+        tile_eff = tile_efficiency(dm[0], G, int(eng.sel.counts[0].to(torch.int64).sum().item()))
+        if dm.shape[0] > 1:  # batch: the tile model of item 0 scaled to the whole shard
+            tile_eff["issued_tile_steps"] = int(round(tile_eff["issued_tile_steps"] * selected /
+                                                      max(tile_eff["useful_group_steps"], 1)))
+            tile_eff["useful_group_steps"] = selected
+        del dm
     except Exception as e:  # noqa: BLE001 - reporting only
         log("tile efficiency unavailable:", e)
-    causal = len(heads) * N * (N + 1) // 2
+    causal = len(shard.batch) * len(heads) * N * (N + 1) // 2
     rho = 1.0 - selected / causal
 
     # ---------------------------------------------------------------- timed region (device)
@@ -408,17 +512,24 @@ def main():
     e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.steps)
     e2e_exact = e2e_exact and bool(torch.equal(Oh.to(eng.O.device), O_ref))
     del O_ref
-    h2d = (Q.numel() + K.numel() + V.numel()) * 2 * world
-    d2h = Q.numel() * 2 * world
+    def sum_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], device="cpu" if args.dist_backend == "gloo" else "cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    h2d = int(sum_over_ranks((Q.numel() + K.numel() + V.numel()) * 2))
+    d2h = int(sum_over_ranks(Q.numel() * 2))
 
     # ---------------------------------------------------------------- NCCL gather (verification only, untimed)
     gather = None
     if dist:
         t0 = time.perf_counter()
         O_loc = eng.O.cpu() if args.dist_backend == "gloo" else eng.O
-        full = gather_heads(O_loc, shards)
+        full = gather_layer(O_loc, shards, args.batch, H)
         torch.cuda.synchronize()
-        sl = full[:, shard.q_heads.start:shard.q_heads.stop]
+        sl = full[shard.batch.start:shard.batch.stop, shard.q_heads.start:shard.q_heads.stop]
         # per-rank selected blocks (max/mean bounds near-linear scaling)
         dev = "cpu" if args.dist_backend == "gloo" else "cuda"
         mine = torch.tensor([float(selected)], device=dev, dtype=torch.float64)
@@ -454,12 +565,15 @@ def main():
         except Exception as e:  # pragma: no cover
             log("cudnn sdpa unavailable:", e)
         try:
-            if not args.flashinfer:
-                raise RuntimeError("skipped (enable with --flashinfer; JIT-compiles on first use)")
+            # flashinfer 0.6.11 single-request prefill on sm100 (backend auto = its FA2
+            # kernels; the trtllm-gen sm100 cubins serve only the paged batch API)
+            if args.no_flashinfer:
+                raise RuntimeError("skipped (--no-flashinfer)")
             import flashinfer
             q3, k3, v3 = Q[0].transpose(0, 1).contiguous(), K[0].transpose(0, 1).contiguous(), V[0].transpose(0, 1).contiguous()
             dense["flashinfer"] = max_over_ranks(timeit(lambda: flashinfer.single_prefill_with_kv_cache(
                 q3, k3, v3, causal=True)))
+            del q3, k3, v3
         except Exception as e:  # pragma: no cover
             log("flashinfer unavailable:", e)
     fastest = min(dense.items(), key=lambda kv: kv[1]) if dense else None
@@ -477,7 +591,7 @@ def main():
                 "issued_tflops": issued_attn / (stage_ms["attention"] * 1e-3) / 1e12 if issued_attn else None}
     else:
         Lq = L // 8
-        fl = 2 * Lq * Lq * len(heads) * d  # compressed_qk (metrics.cpp:60), post-softmax full square
+        fl = 2 * Lq * Lq * len(heads) * len(shard.batch) * d  # compressed_qk (metrics.cpp:60), post-softmax full square
         achieved = fl / (stage_ms["proxy"] * 1e-3) / 1e12
         roof = {"kernel": "proxy_kernel (tcgen05 fp16x3)", "bound": "tensor", "achieved": achieved, "peak": tf_sust,
                 "unit": "TFLOP/s", "frac": achieved / tf_sust,
@@ -488,7 +602,7 @@ def main():
     if os.path.exists(tp):
         roof["traffic"] = json.load(open(tp)).get(args.config, {}).get(roof["kernel"].split()[0])
     roof["peak_source"] = f"MEASURED_PEAKS.json ({peak_src}, sustained bf16)"
-    comp_bytes = (len(heads) + shard.H_kv) * L * d * 2 + (len(heads) + shard.H_kv) * (L // 8) * d * 4
+    comp_bytes = len(shard.batch) * ((len(heads) + shard.H_kv) * L * d * 2 + (len(heads) + shard.H_kv) * (L // 8) * d * 4)
     stage_roofs = {
         "compress": {"bound": "hbm", "bytes": comp_bytes,
                      "achieved_gbs": comp_bytes / (stage_ms["compress"] * 1e-3) / 1e9, "peak_gbs": hbm},
@@ -498,13 +612,13 @@ def main():
     # proxy (+ finalize): compressed_qk (metrics.cpp:60) over the post-softmax full square; the
     # tensor pipe issues it three times (fp16x3 hi.hi + hi.lo + lo.hi)
     cq, ck, ch = cfg.c_q, cfg.c_k, cfg.c_h
-    qk = 2 * (L // cq) * (L // ck) * (len(heads) // ch) * d
+    qk = 2 * (L // cq) * (L // ck) * (len(heads) // ch) * len(shard.batch) * d
     # MUFU floor: ex2 at 16 results / clock / SM (B300_MICROARCH, measured here by
     # tools/ex2_rate.py) at the sustained clock; the proxy exponentiates every logit of the
     # full square (softmax_aggregation / 4 exps, metrics.cpp:62), the attention kernel 7/8 of
     # its issued P entries (1/8 go to the FMA-pipe polynomial)
     mufu_per_s = 16 * 148 * (clk["sm_mhz"] or 1965.0) * 1e6
-    n_exp_proxy = (L // cq) * (L // ck) * (len(heads) // ch)
+    n_exp_proxy = (L // cq) * (L // ck) * (len(heads) // ch) * len(shard.batch)
     stage_roofs["proxy"] = {"bound": "tensor", "flops": qk,
                             "achieved_tflops": qk / (stage_ms["proxy"] * 1e-3) / 1e12,
                             "issued_tflops": 3 * qk / (stage_ms["proxy"] * 1e-3) / 1e12, "peak_tflops": tf_sust,
@@ -518,6 +632,12 @@ def main():
         if dist:
             dist.destroy_process_group()
         return
+    parity = None
+    if not args.no_parity:
+        try:
+            parity = parity_sample(Q, K, V, eng, mode, sel, P)
+        except Exception as e:  # noqa: BLE001 - report, never hide
+            parity = {"error": repr(e)}
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample, info = cpu_sample(args.config, gain, P)
@@ -532,7 +652,7 @@ def main():
                roofline=roof, cpu_baseline=cpu,
                stages_ms=stage_ms, stage_roofline=stage_roofs,
                sparsity={"rho": rho, "selected_blocks": selected, "causal_blocks": causal, "attn_tiles": tile_eff},
-               dense_baselines_ms=dense, verify_gather=gather,
+               dense_baselines_ms=dense, verify_gather=gather, parity=parity,
                speedup_vs_dense={"vs": fastest[0], "dense_ms": fastest[1], "speedup": fastest[1] / ms} if fastest else None)
     print(json.dumps(out), flush=True)
     if dist:

@@ -88,6 +88,10 @@ typedef struct us_params {
   int32_t top_k;       /* k for US_SELECT_TOP_K */
   int32_t flags;       /* US_FLAG_* */
   uint64_t seed;       /* stochastic pooling seed (unused by Mean) */
+  int32_t head0;       /* global index of this call's first Q head (0 for a whole layer): a
+                          call on a head range [head0, head0 + H) of a larger layer (head
+                          sharding, chunked pipelines) seeds stochastic pooling with the
+                          global head index, as the reference does (compression.cpp:17-20) */
 } us_params;
 
 /* Selection outputs (device pointers; every field except mask_bits may be NULL).

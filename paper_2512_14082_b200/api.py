@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import functools
 import math
 import os
 import threading
@@ -60,7 +61,7 @@ class UsParams(C.Structure):
                 ("d_k", C.c_int32), ("S", C.c_int32), ("c_q", C.c_int32), ("c_k", C.c_int32),
                 ("c_h", C.c_int32), ("strategy", C.c_int32), ("causal_mode", C.c_int32),
                 ("select_mode", C.c_int32), ("P", C.c_double), ("top_k", C.c_int32),
-                ("flags", C.c_int32), ("seed", C.c_uint64)]
+                ("flags", C.c_int32), ("seed", C.c_uint64), ("head0", C.c_int32)]
 
 
 class UsSelection(C.Structure):
@@ -158,12 +159,14 @@ def _ptr(t: Optional[torch.Tensor]):
 
 
 def make_params(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64,
-                sync_check: bool = False) -> UsParams:
+                sync_check: bool = False, head0: int = 0) -> UsParams:
+    """head0: global index of Q's first head when Q/K/V are a head range of a larger
+    layer (head sharding): stochastic pooling seeds with the global head index."""
     B, H, L, d = _bhld(Q)
     H_kv = _bhld(K)[1]
     return UsParams(B, H, H_kv, L, d, S, cfg.c_q, cfg.c_k, cfg.c_h, cfg.strategy, cfg.causal_mode,
                     cfg.select_mode, float(cfg.P), cfg.top_k, FLAG_SYNC_CHECK if sync_check else 0,
-                    cfg.seed)
+                    cfg.seed, head0)
 
 
 def _bhld(x: torch.Tensor):
@@ -174,8 +177,26 @@ def _bhld(x: torch.Tensor):
     return tuple(x.shape)
 
 
+def _on_input_device(fn):
+    """Run an operator with Q's device as the current device, so the selection
+    buffers, the workspace and the launch stream all live on the inputs' GPU."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        t = next((a for a in args if isinstance(a, torch.Tensor)), None)
+        if t is not None and t.is_cuda:
+            with torch.cuda.device(t.device):
+                return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+    return wrapper
+
+
 def _check_inputs(*ts: torch.Tensor):
+    dev = None
     for t in ts:
+        if t.is_cuda:
+            if dev is not None and t.device != dev:
+                raise ValueError(f"inputs live on different devices ({dev} and {t.device})")
+            dev = t.device
         if not t.is_cuda:
             raise ValueError("inputs must be CUDA tensors (the GPU path has no CPU fallback)")
         if t.dtype != torch.bfloat16:
@@ -289,6 +310,7 @@ def make_report(p: UsParams, sel: Selection) -> SparsityReport:
 
 
 # ------------------------------------------------------------------ operators
+@_on_input_device
 def compress(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64):
     """compress (compression.cpp:5-25): f32 Qc [B,H/c_h,L/c_q,d], Kc [B,H/c_h,L/c_k,d]."""
     _check_inputs(Q, K)
@@ -301,6 +323,7 @@ def compress(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 
     return Qc, Kc
 
 
+@_on_input_device
 def select_blocks(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 64,
                   with_scores: bool = False, with_indices: bool = False,
                   sync_check: bool = True, proxy: int = PROXY_UNISPARSE, stride: int = 8) -> SparsityReport:
@@ -326,6 +349,7 @@ def select_blocks(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: i
     return rep
 
 
+@_on_input_device
 def build_block_mask(scores: torch.Tensor, cfg: CompressionConfig, H: Optional[int] = None,
                      S: int = 64, with_indices: bool = False) -> Selection:
     """build_block_mask (selection.cpp:60-88) on f32 block scores [B, planes, N, N]."""
@@ -345,6 +369,7 @@ def build_block_mask(scores: torch.Tensor, cfg: CompressionConfig, H: Optional[i
     return sel
 
 
+@_on_input_device
 def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: int = 1, S: int = 64,
                            validate_mask: bool = True, with_lse: bool = True):
     """block_sparse_attention (attention.cpp:89-137). mask_bits: int32 [B, planes, N, W]."""
@@ -360,6 +385,7 @@ def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: in
     return O, lse
 
 
+@_on_input_device
 def unisparse_attn(Q, K, V, cfg: CompressionConfig, S: int = 64, with_scores: bool = False,
                    with_indices: bool = False, sync_check: bool = True) -> UniSparseResult:
     """unisparse_attn (pipeline.cpp:19-24)."""
@@ -376,6 +402,7 @@ def unisparse_attn(Q, K, V, cfg: CompressionConfig, S: int = 64, with_scores: bo
     return UniSparseResult(O=O, lse=lse, report=make_report(p, sel))
 
 
+@_on_input_device
 def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True):
     """Causal dense attention via the same kernel with every causal block selected."""
     _check_inputs(Q, K, V)
@@ -392,10 +419,14 @@ class Engine:
     """Allocation-free repeated calls (bench / serving): params, workspace and
     selection buffers are created once; run() only launches kernels."""
 
-    def __init__(self, Q, K, V, cfg: CompressionConfig, S: int = 64):
+    def __init__(self, Q, K, V, cfg: CompressionConfig, S: int = 64, head0: int = 0):
         _check_inputs(Q, K, V)
-        self.p = make_params(Q, K, cfg, S)
-        self.ws = workspace(self.p)
+        self.device = Q.device
+        self.p = make_params(Q, K, cfg, S, head0=head0)
+        # a private workspace: run_host() uses it on the engine's own streams, so it
+        # must not be shared with other engines or functional calls on this stream
+        self.ws = torch.empty(max(int(lib().us_workspace_bytes(C.byref(self.p))), 256), dtype=torch.uint8,
+                              device=Q.device)
         self.sel = _alloc_selection(self.p, False, False)
         self.ss = _sel_struct(self.sel)
         self.O = torch.empty_like(Q)
@@ -404,6 +435,10 @@ class Engine:
         self.Q, self.K, self.V = Q, K, V
 
     def run(self, dense: bool = False):
+        with torch.cuda.device(self.device):
+            return self._run(dense)
+
+    def _run(self, dense: bool = False):
         if dense:
             _raise(lib().us_dense_attention(C.byref(self.p), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
                                             _ptr(self.O), _ptr(self.lse), None, 0, _stream()))
@@ -431,9 +466,9 @@ class Engine:
         N = p.L // p.S
         W = (N + 31) // 32
         for n in sizes:
-            cp = UsParams(1, n * G, n, p.L, p.d_k, p.S, p.c_q, p.c_k, p.c_h, p.strategy, p.causal_mode,
-                          p.select_mode, p.P, p.top_k, p.flags, p.seed)
             q0, q1 = kv0 * G, (kv0 + n) * G
+            cp = UsParams(1, n * G, n, p.L, p.d_k, p.S, p.c_q, p.c_k, p.c_h, p.strategy, p.causal_mode,
+                          p.select_mode, p.P, p.top_k, p.flags, p.seed, p.head0 + q0)
             pl0, pl1 = q0 // p.c_h, q1 // p.c_h
             sel = UsSelection(self.sel.mask_bits[0, pl0:pl1].data_ptr(), self.sel.counts[0, pl0:pl1].data_ptr(),
                               self.sel.coverage[0, pl0:pl1].data_ptr(), None, None)
@@ -442,6 +477,10 @@ class Engine:
         return plan
 
     def run_host(self, Qh, Kh, Vh, Oh, chunks: int = 4, wait: bool = True):
+        with torch.cuda.device(self.device):
+            return self._run_host(Qh, Kh, Vh, Oh, chunks, wait)
+
+    def _run_host(self, Qh, Kh, Vh, Oh, chunks: int = 4, wait: bool = True):
         """unisparse_attn from (pinned) host buffers: H2D of Q/K/V, the hot path,
         D2H of O, pipelined over KV-head chunks on three CUDA streams (copy-in,
         compute, copy-out) so the PCIe transfers overlap the kernels. Enqueues

@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "libunisparse_b200.so")
-SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "attention2.cu", "lastblock.cu", "io.cu", "metrics.cu", "selftest.cu"]
+SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "attention_kt.cu", "attention2.cu", "lastblock.cu", "io.cu", "metrics.cu", "selftest.cu"]
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

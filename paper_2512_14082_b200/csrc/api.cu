@@ -77,6 +77,7 @@ Checked check(const us_params& p, bool need_compression) {
   if (p.H > 0 && p.H_kv > 0 && p.H % p.H_kv != 0)
     e.push_back("H=" + std::to_string(p.H) + " not divisible by H_kv=" + std::to_string(p.H_kv));
   if (p.B <= 0) e.push_back("B must be positive");
+  if (p.head0 < 0) e.push_back("head0 must be non-negative");
   if (p.select_mode != US_SELECT_TOP_P && p.select_mode != US_SELECT_TOP_K)
     e.push_back("unknown select_mode");
   if (p.select_mode == US_SELECT_TOP_K && p.top_k < 1) e.push_back("top_k must be positive");
@@ -221,12 +222,12 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   Ws w = layout(p);
   US_CUDA_TRY(cudaMemsetAsync(ws, 0, w.header_bytes, st), "workspace clear");
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p.c_q, g.Hc, p.c_h, 1,
-                  at<float>(ws, w.qc), at<uint32_t>(ws, w.absmax_q), p.strategy, 0, p.seed};
+                  at<float>(ws, w.qc), at<uint32_t>(ws, w.absmax_q), p.strategy, 0, p.seed, p.head0};
   us_status s = launch_compress(cq, st);
   if (s != US_OK) return s;
   CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p.c_k, g.kv_planes,
                   g.kv_dedup ? 1 : p.c_h, g.kv_dedup ? 1 : g.G, at<float>(ws, w.kc),
-                  at<uint32_t>(ws, w.absmax_k), p.strategy, 1, p.seed};
+                  at<uint32_t>(ws, w.absmax_k), p.strategy, 1, p.seed, p.head0};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
   SplitArgs sq{at<float>(ws, w.qc), g.B * g.Hc, g.Lq, g.D, at<uint32_t>(ws, w.absmax_q),
                at<int>(ws, w.exp_q), at<__half>(ws, w.qh), at<__half>(ws, w.ql)};
@@ -555,10 +556,10 @@ us_status us_compress(const us_params* p, const void* Q, const void* K, float* Q
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // reference layout: H/c_h planes for both Q and K (K expanded to H heads first)
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p->c_q, g.Hc, p->c_h, 1, Qc, nullptr,
-                  p->strategy, 0, p->seed};
+                  p->strategy, 0, p->seed, p->head0};
   if ((s = launch_compress(cq, st)) != US_OK) return s;
   CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p->c_k, g.Hc, p->c_h, g.G, Kc, nullptr,
-                  p->strategy, 1, p->seed};
+                  p->strategy, 1, p->seed, p->head0};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "compress");
   return US_OK;

@@ -643,12 +643,9 @@ template <int D, int NT>
 us_status launch_attn_t(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                         const CUtensorMap& tmV, cudaStream_t st) {
   const int smem = AttnSmem<D, NT>::kBytes + 1024;  // + alignment slack
-  static bool attr_set = false;
-  if (!attr_set) {
-    US_CUDA_TRY(cudaFuncSetAttribute(attn_kernel<D, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                "attn_kernel smem attribute");
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (us_status s = ensure_smem_attr(attn_kernel<D, NT>, smem, attr_done, "attn_kernel smem attribute"); s != US_OK)
+    return s;
   long long items;
   if (NT == 1) {
     const int G = a.H / a.H_kv;

@@ -447,12 +447,9 @@ __global__ void __launch_bounds__(256, 1)
 template <int D>
 us_status launch_attn2_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st) {
   const int smem = Attn2Smem<D>::kBytes + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    US_CUDA_TRY(cudaFuncSetAttribute(attn2_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                "attn2_kernel smem attribute");
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (us_status s = ensure_smem_attr(attn2_kernel<D>, smem, attr_done, "attn2_kernel smem attribute"); s != US_OK)
+    return s;
   long long items;
   if (a.group_mode != 2) items = (long long)a.B * (a.H / 2) * a.N;
   else items = (long long)a.B * a.H * ((a.N + 1) / 2);

@@ -630,12 +630,14 @@ us_status launch_attention_kt(const AttnArgs& a, const CUtensorMap& tmQ3, const 
     return (e && std::atoi(e) == 2) ? 2 : 4;
   }();
   if (ncg == 2) {
-    US_CUDA_TRY(cudaFuncSetAttribute(attn_kt_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                "attn_kt_kernel smem attribute");
+    static std::atomic<uint64_t> attr_done{0};
+    if (us_status s = ensure_smem_attr(attn_kt_kernel<2>, smem, attr_done, "attn_kt_kernel smem attribute"); s != US_OK)
+      return s;
     attn_kt_kernel<2><<<grid, 32 * (4 + 4 * 2), smem, st>>>(tmQ3, tmK2, tmV3, a);
   } else {
-    US_CUDA_TRY(cudaFuncSetAttribute(attn_kt_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                "attn_kt_kernel smem attribute");
+    static std::atomic<uint64_t> attr_done{0};
+    if (us_status s = ensure_smem_attr(attn_kt_kernel<4>, smem, attr_done, "attn_kt_kernel smem attribute"); s != US_OK)
+      return s;
     attn_kt_kernel<4><<<grid, 32 * (4 + 4 * 4), smem, st>>>(tmQ3, tmK2, tmV3, a);
   }
   US_LAUNCH_CHECK("attn_kt_kernel");

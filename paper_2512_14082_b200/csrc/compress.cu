@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double in
         // stochastic (compression.hpp:33-53): pick window row r with probability
         // |row r| / sum of row norms, drawn from CounterRng(chain(chain(seed, role, h), t)).
         // Row norms: fp64 sums of squares (exact for bf16 inputs), sqrt, summed in row order.
-        uint64_t state = chain_seed(chain_seed(chain_seed(a.seed, uint64_t(a.role)), uint64_t(h)), uint64_t(t));
+        uint64_t state = chain_seed(chain_seed(chain_seed(a.seed, uint64_t(a.role)), uint64_t(a.head0 + h)), uint64_t(t));
         auto row_norm = [&](int rr) {
           const uint4 v = ld_stream(src + rr * stride);
           const uint32_t w[4] = {v.x, v.y, v.z, v.w};

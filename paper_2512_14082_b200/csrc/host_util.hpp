@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
@@ -35,6 +36,20 @@ inline us_status cuda_status(cudaError_t e, const char* what) {
     us_status _s = ::us::cuda_status(cudaGetLastError(), what);   \
     if (_s != US_OK) return _s;                                   \
   } while (0)
+
+// Dynamic shared memory above 48 KB is a per-DEVICE function attribute: set it once
+// per device ordinal (bit d of `done`; devices >= 64 set it on every launch). Two
+// threads racing on the same device both set the same value, which is harmless.
+template <typename Kernel>
+inline us_status ensure_smem_attr(Kernel* fn, int bytes, std::atomic<uint64_t>& done, const char* what) {
+  int dev = 0;
+  US_CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+  const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return US_OK;
+  US_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), what);
+  done.fetch_or(bit, std::memory_order_release);
+  return US_OK;
+}
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

@@ -30,6 +30,7 @@ struct CompressArgs {
   int strategy;    // US_POOL_MEAN / MAX / STOCHASTIC (compression.hpp:24-53)
   int role;        // stochastic seed tag: 0 = Q, 1 = K (compression.cpp:17-20)
   uint64_t seed;   // CompressionConfig::seed
+  int head0;       // global index of the call's first head (stochastic seeds use head0 + h)
 };
 us_status launch_compress(const CompressArgs& a, cudaStream_t st);
 

@@ -351,13 +351,11 @@ us_status launch_block_recall(int B, int H, int N, int W, int planes, int heads_
 
 us_status launch_row_spearman(int B, int H, int N, int c_h, const float* proxy, const float* ref, double* rows_ws,
                               uint8_t* defined, double* out, long long* n_def, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    US_CUDA_TRY(cudaFuncSetAttribute(spearman_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kSpearmanSmem)),
-                "spearman_rows_kernel smem attribute");
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (us_status s = ensure_smem_attr(spearman_rows_kernel, int(kSpearmanSmem), attr_done,
+                                     "spearman_rows_kernel smem attribute");
+      s != US_OK)
+    return s;
   SpearmanArgs a{B, H, N, c_h, proxy, ref, rows_ws, defined};
   spearman_rows_kernel<<<unsigned((long long)B * H * N), kThreads, kSpearmanSmem, st>>>(a);
   US_LAUNCH_CHECK("spearman_rows_kernel");

@@ -346,12 +346,8 @@ template <int D, int SW, bool X3>
 us_status launch_proxy_x(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
   const int smem = ProxySmem<D>::kBytes + 1024;
   auto kern = proxy_kernel<D, SW, X3>;
-  static bool attr_set = false;  // benign race: idempotent attribute set
-  if (!attr_set) {
-    US_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                "proxy_kernel smem attribute");
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (us_status s = ensure_smem_attr(kern, smem, attr_done, "proxy_kernel smem attribute"); s != US_OK) return s;
   dim3 grid((a.Lq + kRows - 1) / kRows, a.Hc, a.B);
   kern<<<grid, 320, smem, st>>>(tmKh, tmKl, a);
   US_LAUNCH_CHECK("proxy_kernel");

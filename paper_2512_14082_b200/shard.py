@@ -10,13 +10,18 @@ K/V head is then replicated on the ranks sharing it — Qwen 28Q/4KV on 8 GPUs:
 7-head groups split 4 + 3). Inside a shard the kernels see an ordinary layer
 with H' Q heads and H'_kv K/V heads, so the hot path has no collective.
 
+Batch items are independent as well: shard_layer() splits the world into
+gcd(world, B) batch parts times world/gcd head parts, so every rank owns a
+(batch range x head range) block of the [B][H][L][d] layer.
+
 NCCL (torch.distributed) is used only to gather the per-rank O slices for
-verification (gather_heads); with the head-major [B][H][L][d] layout the gather
-is a concatenation along the head dimension.
+verification (gather_heads / gather_layer); with the head-major [B][H][L][d]
+layout the gather is a placement of (batch, head) blocks.
 """
 from __future__ import annotations
 
 import dataclasses
+import math
 from typing import List
 
 
@@ -25,6 +30,7 @@ class Shard:
     rank: int
     q_heads: range    # global Q heads owned by this rank
     kv_heads: range   # global K/V heads they read
+    batch: range = range(0, 1)  # batch items owned by this rank (shard_layer)
 
     @property
     def H(self) -> int:
@@ -78,6 +84,45 @@ def shard_heads(H: int, H_kv: int, world: int, c_h: int = 1) -> List[Shard]:
             h0 += n * c_h
             r += 1
     return shards
+
+
+def shard_layer(B: int, H: int, H_kv: int, world: int, c_h: int = 1) -> List[Shard]:
+    """Partition a [B][H] layer over `world` ranks by (batch, KV-head group): the
+    world splits into bp = gcd(world, B) batch parts x hp = world / bp head parts
+    (shard_heads over hp ranks); rank r owns batch part r // hp, head part r % hp.
+    No collective is needed on the hot path (batch items and KV groups never couple)."""
+    if B <= 0:
+        raise ValueError("B must be positive")
+    if world <= 0:
+        raise ValueError("world size must be positive")
+    bp = math.gcd(world, B)
+    hp = world // bp
+    heads = shard_heads(H, H_kv, hp, c_h)
+    per_b = B // bp
+    out = []
+    for r in range(world):
+        hs = heads[r % hp]
+        b0 = (r // hp) * per_b
+        out.append(Shard(r, hs.q_heads, hs.kv_heads, range(b0, b0 + per_b)))
+    return out
+
+
+def gather_layer(local, shards: List[Shard], B: int, H: int, group=None):
+    """All-gather per-rank [B_r][H_r][...] blocks into the full [B][H][...] tensor
+    (verification only). Blocks are padded to the largest shard for the collective."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    Bm = max(len(s.batch) for s in shards)
+    Hm = max(s.H for s in shards)
+    pad = torch.zeros((Bm, Hm) + tuple(local.shape[2:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0], : local.shape[1]] = local
+    tmp = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(tmp, pad.contiguous(), group=group)
+    full = torch.empty((B, H) + tuple(local.shape[2:]), dtype=local.dtype, device=local.device)
+    for t, s in zip(tmp, shards):
+        full[s.batch.start:s.batch.stop, s.q_heads.start:s.q_heads.stop] = t[: len(s.batch), : s.H]
+    return full
 
 
 def imbalance(shards: List[Shard]) -> float:

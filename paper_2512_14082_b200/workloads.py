@@ -19,16 +19,17 @@ import torch
 @torch.no_grad()
 def planted_blocks(L: int, H: int, H_kv: int, d: int, S: int = 64, *, seed: int = 0,
                    gain: float = 9.0, m: int = 2, sigma: float = 0.1, heads=None, B: int = 1,
-                   device="cuda", dtype=torch.bfloat16):
-    """Returns Q [B, len(heads), L, d], K/V [B, n_kv, L, d] for the requested Q heads
-    (default all) and the KV heads they read; the planted structure of head h
-    depends only on (seed, b, h), so head shards agree with the full tensor."""
+                   batches=None, device="cuda", dtype=torch.bfloat16):
+    """Returns Q [len(batches), len(heads), L, d], K/V [len(batches), n_kv, L, d] for
+    the requested batch items (default range(B)) and Q heads (default all) and the
+    KV heads they read; the planted structure of (b, h) depends only on (seed, b, h),
+    so (batch, head) shards agree with the full tensor."""
     heads = list(range(H)) if heads is None else list(heads)
     G = H // H_kv
     kv_heads = sorted({h // G for h in heads})
     N = L // S
     Qs, Ks, Vs = [], [], []
-    for b in range(B):
+    for b in (range(B) if batches is None else batches):
         q = torch.empty((len(heads), L, d), device=device, dtype=torch.float32)
         k = torch.empty((len(kv_heads), L, d), device=device, dtype=torch.float32)
         v = torch.empty((len(kv_heads), L, d), device=device, dtype=torch.float32)

@@ -93,3 +93,62 @@ def test_gloo_world2_gather_equals_single_process(tmp_path, H, H_kv, c_h):
     Or, _, mask, _ = O.unisparse_attn(O.cfg(H, L, d, S, H_kv=H_kv, c_h=c_h, P=0.9), Q, K, V)
     assert np.array_equal(got["mask"].astype(bool), mask)
     assert np.array_equal(got["O"], Or)
+
+
+# ------------------------------------------------------------------ (batch x head) partitioning
+from paper_2512_14082_b200.shard import gather_layer, shard_layer  # noqa: E402
+
+
+@pytest.mark.parametrize("B,H,H_kv,world,bparts", [
+    (1, 32, 8, 8, 1), (2, 32, 8, 8, 2), (4, 32, 8, 8, 4), (8, 32, 8, 8, 8), (8, 32, 8, 2, 2),
+    (3, 28, 4, 6, 3), (6, 40, 40, 4, 2), (2, 28, 4, 8, 2),
+])
+def test_shard_layer_covers_batch_x_heads(B, H, H_kv, world, bparts):
+    sh = shard_layer(B, H, H_kv, world)
+    assert len(sh) == world
+    cells = {(b, h) for s in sh for b in s.batch for h in s.q_heads}
+    assert cells == {(b, h) for b in range(B) for h in range(H)}
+    assert sum(len(s.batch) * s.H for s in sh) == B * H  # no (b, h) owned twice
+    assert len({(s.batch.start, s.batch.stop) for s in sh}) == bparts
+    G = H // H_kv
+    for s in sh:
+        assert all(h // G in s.kv_heads for h in s.q_heads)
+
+
+def _layer_worker(rank, world, port, B, H, H_kv, out_path):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sh = shard_layer(B, H, H_kv, world)
+    s = sh[rank]
+    full_ref = torch.arange(B * H * 3, dtype=torch.float32).reshape(B, H, 3)
+    local = full_ref[s.batch.start:s.batch.stop, s.q_heads.start:s.q_heads.stop].contiguous()
+    full = gather_layer(local, sh, B, H)
+    if rank == 0:
+        torch.save({"got": full, "ref": full_ref}, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B,H,H_kv,world", [(2, 8, 2, 2), (1, 8, 2, 2), (3, 6, 3, 2)])
+def test_gloo_gather_layer(tmp_path, B, H, H_kv, world):
+    import torch
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "layer.pt")
+    mp.spawn(_layer_worker, args=(world, _free_port(), B, H, H_kv, out), nprocs=world, join=True)
+    d = torch.load(out)
+    assert torch.equal(d["got"], d["ref"])
+
+
+def test_bench_rejects_world_mismatch():
+    """bench.py --gpus N under a launcher that started a different number of ranks
+    must fail (n_gpus is the world size the line reports)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--no-cpu"],
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0
+    assert "--gpus 2 but WORLD_SIZE=1" in (r.stderr + r.stdout)
