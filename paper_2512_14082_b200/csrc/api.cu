@@ -160,7 +160,10 @@ struct Ws {
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
-Ws layout(const us_params& p) {
+// scores_region: the [B][planes][N][N] f32 block-score tensor, needed only by the
+// competitor proxies and exact_block_mass; the UniSparse path fuses the block
+// scores into the selection (select_fused_kernel) and never materialises them.
+Ws layout(const us_params& p, bool scores_region = false) {
   Geo g(p);
   Ws w{};
   size_t o = 0;
@@ -194,7 +197,7 @@ Ws layout(const us_params& p) {
   const size_t ns = 128 / size_t(proxy_slot_width(g.rk));
   w.part = take(4 * qplanes * T * g.Lq * ns);
   w.tmax = take(4 * qplanes * T * g.Lq);
-  w.scores = take(4 * rows * g.N);
+  w.scores = scores_region ? take(4 * rows * g.N) : 0;
   w.mask = take(4 * rows * g.W);
   w.total = o;
   return w;
@@ -205,9 +208,8 @@ T* at(void* ws, size_t off) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + off);
 }
 
-us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, size_t* need_out = nullptr) {
-  const size_t need = layout(p).total;
-  if (need_out) *need_out = need;
+us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, bool scores_region = false) {
+  const size_t need = layout(p, scores_region).total;
   if (!ws || bytes < need) {
     set_error(std::string(who) + ": workspace of " + std::to_string(need) + " bytes required");
     return US_ERR_WORKSPACE;
@@ -215,9 +217,10 @@ us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, s
   return US_OK;
 }
 
-// compress + split + proxy (pass 1, 2) into ws.scores.
+// compress + split + proxy (logits, row LSE, slot partials). The block scores are
+// formed by the fused selection (launch_select_fused with *pa_out).
 us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, cudaStream_t st,
-                    int prof_call = -1) {
+                    ProxyArgs* pa_out, int prof_call = -1) {
   Geo g(p);
   Ws w = layout(p);
   US_CUDA_TRY(cudaMemsetAsync(ws, 0, w.header_bytes, st), "workspace clear");
@@ -265,9 +268,11 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   pa.part = at<float>(ws, w.part);
   pa.tmax = at<float>(ws, w.tmax);
   pa.lse2 = at<float>(ws, w.lse2);
-  pa.scores = at<float>(ws, w.scores);
+  pa.scores = nullptr;
   pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
   pa.x3 = 1;
+  pa.finalize = 0;
+  *pa_out = pa;
   return launch_proxy(pa, tKh, tKl, st);
 }
 
@@ -290,7 +295,7 @@ us_status run_antidiagonal(const us_params& p, int stride, const void* Q, const 
                            cudaStream_t st) {
   const us_params q = antidiag_params(p, stride);
   Geo g(q);
-  Ws w = layout(q);
+  Ws w = layout(q, true);
   const int Lc = g.L / stride;
   CUtensorMap tK;
   EncodeTiledFn fn = encode_tiled_fn();
@@ -333,6 +338,7 @@ us_status run_antidiagonal(const us_params& p, int stride, const void* Q, const 
   pa.tmax = at<float>(ws, w.tmax);
   pa.lse2 = at<float>(ws, w.lse2);
   pa.scores = at<float>(ws, w.scores);
+  pa.finalize = 1;
   pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
   pa.x3 = 0;
   pa.qraw = static_cast<const uint16_t*>(Q);
@@ -371,6 +377,29 @@ us_status run_select_rows(const us_params& p, const float* scores, int planes, u
   sa.fb_count = at<int32_t>(ws, w.fb_count);
   sa.fb_rows = at<int32_t>(ws, w.fb_rows);
   return launch_select(sa, st);
+}
+
+// Fused finalize + selection on the proxy's slot partials (the UniSparse path).
+us_status run_select_fused(const us_params& p, const ProxyArgs& pa, uint32_t* mask, const us_selection* sel, void* ws,
+                           cudaStream_t st) {
+  Geo g(p);
+  Ws w = layout(p);
+  SelectArgs sa{};
+  sa.scores_out = sel ? sel->scores : nullptr;  // raw block scores only when asked for
+  sa.rows = g.B * g.Hc * g.N;
+  sa.N = g.N;
+  sa.W = g.W;
+  sa.select_mode = p.select_mode;
+  sa.P = p.P;
+  sa.top_k = p.top_k;
+  sa.mask_bits = mask;
+  sa.counts = sel ? sel->counts : nullptr;
+  sa.coverage = sel ? sel->coverage : nullptr;
+  sa.indices = sel ? sel->indices : nullptr;
+  sa.err = at<uint32_t>(ws, w.err);
+  sa.fb_count = at<int32_t>(ws, w.fb_count);
+  sa.fb_rows = at<int32_t>(ws, w.fb_rows);
+  return launch_select_fused(pa, sa, st);
 }
 
 // Attention kernel selection (calibration knob, US_ATTN_IMPL): 0 = automatic
@@ -573,22 +602,18 @@ us_status us_select(const us_params* p, const void* Q, const void* K, const us_s
   Geo g(*p);
   Ws w = layout(*p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((s = run_proxy(*p, Q, K, workspace, st)) != US_OK) return s;
-  if (out && out->scores)
-    US_CUDA_TRY(cudaMemcpyAsync(out->scores, at<float>(workspace, w.scores),
-                                size_t(4) * g.B * g.Hc * g.N * g.N, cudaMemcpyDeviceToDevice, st),
-                "scores copy");
+  ProxyArgs pa{};
+  if ((s = run_proxy(*p, Q, K, workspace, st, &pa)) != US_OK) return s;
   uint32_t* mask = (out && out->mask_bits) ? out->mask_bits : at<uint32_t>(workspace, w.mask);
-  if ((s = run_select_rows(*p, at<float>(workspace, w.scores), g.Hc, mask, out, workspace, st)) != US_OK)
-    return s;
+  if ((s = run_select_fused(*p, pa, mask, out, workspace, st)) != US_OK) return s;
   if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "select_blocks");
   return US_OK;
 }
 
 size_t us_proxy_workspace_bytes(const us_params* p, int32_t proxy, int32_t stride) {
   if (!p || !check(*p, false).errors.empty()) return 0;
-  if (proxy == US_PROXY_ANTIDIAGONAL && stride > 0) return layout(antidiag_params(*p, stride)).total;
-  if (proxy == US_PROXY_LAST_BLOCK) return layout(antidiag_params(*p, p->S)).total;
+  if (proxy == US_PROXY_ANTIDIAGONAL && stride > 0) return layout(antidiag_params(*p, stride), true).total;
+  if (proxy == US_PROXY_LAST_BLOCK) return layout(antidiag_params(*p, p->S), true).total;
   return layout(*p).total;
 }
 
@@ -602,9 +627,9 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
     // layout of one composite row per block (c = S); the chunk statistics, row LSE
     // and column masses live in its (large) slot-partial region.
     const us_params q = antidiag_params(*p, p->S);
-    if ((s = need_ws(q, workspace, workspace_bytes, "select_blocks")) != US_OK) return s;
+    if ((s = need_ws(q, workspace, workspace_bytes, "select_blocks", true)) != US_OK) return s;
     Geo g(q);
-    Ws w = layout(q);
+    Ws w = layout(q, true);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
     LastBlockArgs la{};
@@ -646,9 +671,9 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
     return US_ERR_UNSUPPORTED;
   }
   const us_params q = antidiag_params(*p, stride);
-  if ((s = need_ws(q, workspace, workspace_bytes, "select_blocks")) != US_OK) return s;
+  if ((s = need_ws(q, workspace, workspace_bytes, "select_blocks", true)) != US_OK) return s;
   Geo g(q);
-  Ws w = layout(q);
+  Ws w = layout(q, true);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
   if ((s = run_antidiagonal(*p, stride, Q, K, workspace, st)) != US_OK) return s;
@@ -665,7 +690,7 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
 // ---------------------------------------------------------------- quality metrics (§8f-4)
 size_t us_mass_workspace_bytes(const us_params* p) {
   if (!p || !check(*p, false).errors.empty()) return 0;
-  return layout(antidiag_params(*p, 1)).total;
+  return layout(antidiag_params(*p, 1), true).total;
 }
 
 us_status us_exact_block_mass(const us_params* p, const void* Q, const void* K, float* mass, void* workspace,
@@ -680,9 +705,9 @@ us_status us_exact_block_mass(const us_params* p, const void* Q, const void* K, 
     return US_ERR_INVALID_ARGUMENT;
   }
   const us_params q = antidiag_params(*p, 1);
-  if ((s = need_ws(q, workspace, workspace_bytes, "exact_block_mass")) != US_OK) return s;
+  if ((s = need_ws(q, workspace, workspace_bytes, "exact_block_mass", true)) != US_OK) return s;
   Geo g(q);
-  Ws w = layout(q);
+  Ws w = layout(q, true);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   US_CUDA_TRY(cudaMemsetAsync(workspace, 0, w.header_bytes, st), "workspace clear");
   if ((s = run_antidiagonal(*p, 1, Q, K, workspace, st)) != US_OK) return s;
@@ -877,15 +902,11 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int call = g_prof.on() ? g_prof.next++ : -1;
   g_prof.mark(call, 0, st);
-  if ((s = run_proxy(*p, Q, K, workspace, st, call)) != US_OK) return s;
+  ProxyArgs pa{};
+  if ((s = run_proxy(*p, Q, K, workspace, st, &pa, call)) != US_OK) return s;
   g_prof.mark(call, 2, st);
-  if (sel && sel->scores)
-    US_CUDA_TRY(cudaMemcpyAsync(sel->scores, at<float>(workspace, w.scores),
-                                size_t(4) * g.B * g.Hc * g.N * g.N, cudaMemcpyDeviceToDevice, st),
-                "scores copy");
   uint32_t* mask = (sel && sel->mask_bits) ? sel->mask_bits : at<uint32_t>(workspace, w.mask);
-  if ((s = run_select_rows(*p, at<float>(workspace, w.scores), g.Hc, mask, sel, workspace, st)) != US_OK)
-    return s;
+  if ((s = run_select_fused(*p, pa, mask, sel, workspace, st)) != US_OK) return s;
   g_prof.mark(call, 3, st);
   if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st)) != US_OK) return s;
   g_prof.mark(call, 4, st);

@@ -73,6 +73,8 @@ struct ProxyArgs {
   int k_phase;         // key phase class (3-D K map: (d, stride, rows/stride))
   int live_bias;       // live keys of composite row r = r + live_bias
   int accumulate;      // finalize adds into scores instead of overwriting
+  int finalize;        // 1: launch the finalize (block scores into `scores`); 0: the caller
+                       //    fuses it into the selection (launch_select_fused)
 };
 int proxy_slot_width(int rk);
 // One pass (logits, row LSE, slot partials) then the finalize (block scores).
@@ -96,6 +98,7 @@ us_status launch_last_block_probe(const LastBlockArgs& a, cudaStream_t st);
 // ---------------------------------------------------------------- selection (a4-a5)
 struct SelectArgs {
   const float* scores;  // [rows][N] (row = (b*planes + p)*N + i), j <= i read
+  float* scores_out;    // fused path: raw block scores written here when non-null
   int rows, N, W;
   int select_mode;
   double P;
@@ -109,6 +112,13 @@ struct SelectArgs {
   int32_t* fb_rows;     // fallback row list [rows]
 };
 us_status launch_select(const SelectArgs& a, cudaStream_t st);
+// Fused finalize + selection (UniSparse path): one CTA per (plane, query block)
+// row builds the row's block scores in shared memory from the proxy's slot
+// partials (proxy_score.cuh), selects by radix descent + fp64 certification, and
+// emits bits / counts / coverage / indices; sa.scores_out (nullable) receives the raw
+// scores when the caller asked for them. Uncertified rows go to the exact
+// sorted-walk fallback, which recomputes the row from the partials.
+us_status launch_select_fused(const ProxyArgs& pa, const SelectArgs& sa, cudaStream_t st);
 
 // ---------------------------------------------------------------- attention (a6)
 struct AttnArgs {

@@ -37,12 +37,13 @@
 #include "host_util.hpp"
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "proxy_score.cuh"
 
 namespace us {
 namespace {
 
 constexpr int kRows = 128;  // composite query rows per CTA (UMMA M)
-constexpr int kKeys = 128;  // composite keys per tile (UMMA N)
+constexpr int kKeys = kProxyKeys;  // composite keys per tile (UMMA N)
 // TMEM columns: S buffers [0,128) and [128,256); Q hi at 256, Q lo at 320 (D/2 cols each).
 constexpr uint32_t kTS0 = 0, kTQh = 256, kTQl = 320;
 
@@ -295,49 +296,21 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-// score(i, j) for j <= i from the slot partials (fixed row order r = 0..rq-1,
-// slots of a key block in ascending order). CTA = (query block i, plane).
-// RQ / SPB > 0: compile-time rows per query block / slots per key block (the
-// c = 8 fast path: every load of a score issued before its first use).
+// score(i, j) for j <= i from the slot partials (proxy_score.cuh). CTA = (query
+// block i, plane). Only used when the scores tensor itself is wanted (competitor
+// proxies, exact block mass); the UniSparse path fuses this into the selection
+// (select.cu, launch_select_fused).
 template <int SW, int RQ, int SPB>
 __global__ void __launch_bounds__(256) proxy_finalize_kernel(const ProxyArgs a) {
-  constexpr int NS = kKeys / SW;
   __shared__ float lse_sh[64];
   const int i = gridDim.x - 1 - blockIdx.x;
   const int plane = blockIdx.y;
   const int rq = RQ > 0 ? RQ : a.rq;
-  const int spb = SPB > 0 ? SPB : a.rk / SW;  // slots per key block
-  const int row0 = i * rq;
-  if (threadIdx.x < rq) lse_sh[threadIdx.x] = a.lse2[(long long)plane * a.Lq + row0 + threadIdx.x];
+  if (threadIdx.x < rq) lse_sh[threadIdx.x] = a.lse2[(long long)plane * a.Lq + i * rq + threadIdx.x];
   __syncthreads();
   float* out = a.scores + ((long long)plane * a.N + i) * a.N;
   for (int j = threadIdx.x; j <= i; j += blockDim.x) {
-    const int key0 = j * a.rk;
-    const int t = key0 / kKeys, s0 = (key0 % kKeys) / SW;
-    const long long base = ((long long)plane * a.T + t) * a.Lq + row0;
-    float acc = 0.f;
-    if (RQ > 0 && SPB > 0) {
-      constexpr int R = RQ > 0 ? RQ : 1;
-      float pm[R], ps[R];
-#pragma unroll
-      for (int r = 0; r < RQ; ++r) {
-        pm[r] = __ldg(a.tmax + base + r);
-        float v = 0.f;
-#pragma unroll
-        for (int u = 0; u < SPB; ++u) v += __ldg(a.part + (base + r) * NS + s0 + u);
-        ps[r] = v;
-      }
-      // (a row with no live key — a competitor proxy's first phase-class row — adds 0)
-#pragma unroll
-      for (int r = 0; r < RQ; ++r) acc += lse_sh[r] == -INFINITY ? 0.f : ps[r] * ex2_approx(pm[r] - lse_sh[r]);
-    } else {
-      for (int r = 0; r < rq; ++r) {
-        const float* pr = a.part + (base + r) * NS + s0;
-        float v = 0.f;
-        for (int u = 0; u < spb; ++u) v += pr[u];
-        acc += lse_sh[r] == -INFINITY ? 0.f : v * ex2_approx(a.tmax[base + r] - lse_sh[r]);
-      }
-    }
+    const float acc = proxy_block_score<SW, RQ, SPB>(a, plane, i, j, lse_sh);
     out[j] = a.accumulate ? out[j] + acc : acc;
   }
 }
@@ -351,6 +324,7 @@ us_status launch_proxy_x(const ProxyArgs& a, const CUtensorMap& tmKh, const CUte
   dim3 grid((a.Lq + kRows - 1) / kRows, a.Hc, a.B);
   kern<<<grid, 320, smem, st>>>(tmKh, tmKl, a);
   US_LAUNCH_CHECK("proxy_kernel");
+  if (!a.finalize) return US_OK;
   const dim3 fgrid(a.N, a.B * a.Hc);
   if (SW == 8 && a.rq == 8 && a.rk == 8) proxy_finalize_kernel<SW, 8, 1><<<fgrid, 256, 0, st>>>(a);
   else proxy_finalize_kernel<SW, 0, 0><<<fgrid, 256, 0, st>>>(a);

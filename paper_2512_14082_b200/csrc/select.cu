@@ -27,6 +27,7 @@
 #include "host_util.hpp"
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "proxy_score.cuh"
 
 namespace us {
 namespace {
@@ -315,6 +316,412 @@ __global__ void __launch_bounds__(256) select_fallback_kernel(SelectArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- fused finalize + selection
+// One CTA (256 threads) per (plane, query block) row, rows heaviest first in a
+// grid-stride loop. The row's scores are built in shared memory from the proxy's
+// slot partials (the block_aggregate of proxy.cpp:48-72, bit-identical to the
+// standalone finalize), never round-tripping through HBM. Selection:
+//   Top-P: radix descent over the value bits (11 + 11 + 9 bits, float mass
+//          histograms in smem) finds the candidate threshold v* with
+//          G(v*) = sum_{x >= v*} x >= T = P * total; then the exact fp64 boundary
+//          walk and the 4 n u total certification of select_row; an uncertified row
+//          goes to the exact sorted walk (select_fallback_fused_kernel).
+//   top-k: the same descent on counts (exact), ties by ascending index.
+constexpr int kFusedThreads = 128;
+constexpr int kFusedWarps = kFusedThreads / 32;
+constexpr int kFusedMaxW = kFbMaxN / 32;
+constexpr int kRadixBins = 256;
+
+__device__ __forceinline__ double block_sum_f64(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum_f64(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kFusedWarps; ++w) t += sh[w];  // fixed order
+  return t;
+}
+__device__ __forceinline__ int block_sum_i32(int v, int* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum_i32(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int w = 0; w < kFusedWarps; ++w) t += sh[w];
+  return t;
+}
+// exclusive prefix over W <= 128 per-word counts (warp 0; the caller syncs)
+__device__ __forceinline__ void word_scan(const int* cnt, int* pre, int W) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int w0 = 0; w0 < W; w0 += 32) {
+      const int v = w0 + lane < W ? cnt[w0 + lane] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (w0 + lane < W) pre[w0 + lane] = base + incl - v;
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+// Dynamic shared memory: the row's scores (N floats) then the radix histogram.
+template <int SW, int RQ, int SPB>
+__global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const ProxyArgs pa, const SelectArgs sa) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  float* sc = reinterpret_cast<float*>(fsm);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(fsm + size_t(sa.N) * 4);
+  __shared__ float lse_sh[64];
+  __shared__ double dsh[kFusedWarps];
+  __shared__ int ish[kFusedWarps];
+  __shared__ int wcnt[kFusedMaxW], wpre[kFusedMaxW];
+  __shared__ uint32_t wbits[kFusedMaxW];
+  __shared__ uint32_t ush[kFusedWarps];
+  __shared__ uint32_t sh_bin, sh_above;
+  __shared__ int sh_ties, sh_cert;
+  __shared__ double sh_cum;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int N = sa.N, W = sa.W;
+  const long long planes = sa.rows / N;
+  const int rq = RQ > 0 ? RQ : pa.rq;
+  for (long long rr = blockIdx.x; rr < sa.rows; rr += gridDim.x) {
+    const int plane = int(rr % planes);
+    const int i = N - 1 - int(rr / planes);
+    const long long row = (long long)plane * N + i;
+    const int n = i + 1;
+    if (tid < rq) lse_sh[tid] = pa.lse2[(long long)plane * pa.Lq + (long long)i * rq + tid];
+    __syncthreads();
+    // ---- scores of the row (raw values to sa.scores_out when requested)
+    double part = 0.0;
+    bool bad = false, nonfinite = false;
+    // four scores per thread in flight (their 4 x 16 partial loads issued together);
+    // indices past the row are clamped for the loads and discarded
+    for (int j0 = tid; j0 < n; j0 += 4 * kFusedThreads) {
+      float fv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) fv[u] = proxy_block_score<SW, RQ, SPB>(pa, plane, i, min(j0 + u * kFusedThreads, n - 1),
+                                                                          lse_sh);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * kFusedThreads;
+        if (j < n) {
+          float f = fv[u];
+          if (sa.scores_out) sa.scores_out[row * N + j] = f;
+          if (!(f >= 0.f)) {
+            bad = true;
+            f = 0.f;
+          }
+          if (f == 0.f) f = 0.f;  // -0 -> +0
+          if (isinf(f)) nonfinite = true;
+          sc[j] = f;
+          part += double(f);
+        }
+      }
+    }
+    bad = __syncthreads_or(bad);
+    nonfinite = __syncthreads_or(nonfinite);
+    if (bad && tid == 0) atomicOr(sa.err, 1u);
+    const double total = block_sum_f64(part, dsh);
+
+    int mode = 0;  // 0: threshold / top-k rule, 1: all, 2: diagonal only
+    uint32_t bstar = 0;
+    int ties_needed = 0, E_sh = 0;
+    bool certified = true;
+    double cum = 0.0;
+    const bool topk = sa.select_mode == US_SELECT_TOP_K;
+    if (!topk) {
+      if (!(total > 0.0)) mode = 2;
+      else if (sa.P >= 1.0) mode = 1;
+      else if (nonfinite) certified = false;
+    }
+    if (mode == 0 && certified) {
+      // ---- radix descent for v*: the largest value whose tail (mass or count)
+      // reaches the target. Mass in u32 fixed point x * 2^fs with the row total
+      // below 2^31 (native shared-memory integer atomics); the candidate is only
+      // approximately ordered against T — certification below decides.
+      const int kk = min(sa.top_k, n);
+      int ex = 0;
+      frexp(total > 0.0 ? total : 1.0, &ex);  // total < 2^ex
+      const int fs = 30 - ex;
+      const double fscale = ldexp(1.0, fs);
+      const float fscale_f = ldexpf(1.0f, fs);  // x * 2^fs < 2^30: exact in fp32
+      const uint32_t target = topk ? uint32_t(kk) : uint32_t(fmin(sa.P * total * fscale, 2147483647.0));
+      uint32_t prefix = 0, pmask = 0, above = 0;
+      // 8-bit digits: bits [30:23] (the exponent), [22:15], [14:7], [6:0]; 256 bins,
+      // two per thread
+#pragma unroll 1
+      for (int pass = 0; pass < 4; ++pass) {
+        const int sh = pass == 0 ? 23 : (pass == 1 ? 15 : (pass == 2 ? 7 : 0));
+        const uint32_t dmask = pass == 3 ? 127u : 255u;
+        hist[tid] = 0u;
+        hist[tid + kFusedThreads] = 0u;
+        __syncthreads();
+        for (int j = tid; j < n; j += kFusedThreads) {
+          const uint32_t x = __float_as_uint(sc[j]);
+          if ((x & pmask) == prefix) atomicAdd(&hist[(x >> sh) & dmask], topk ? 1u : uint32_t(sc[j] * fscale_f));
+        }
+        __syncthreads();
+        // exclusive suffix over threads of their two bins: warp suffix scan, then the warps above
+        const uint32_t h0 = hist[2 * tid], h1 = hist[2 * tid + 1];
+        const uint32_t loc = h0 + h1;
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_down_sync(0xffffffffu, incl, o);
+          if (lane + o < 32) incl += y;
+        }
+        if (lane == 0) ush[wid] = incl;
+        if (tid == 0) {
+          sh_bin = 0;
+          sh_above = above;
+        }
+        __syncthreads();
+        uint32_t acc = above + (incl - loc);
+#pragma unroll
+        for (int w = kFusedWarps - 1; w > 0; --w)
+          if (w > wid) acc += ush[w];
+        // bins 2 tid + 1 (upper) then 2 tid: the crossing bin (at most one thread)
+        if (acc < target && acc + h1 >= target) {
+          sh_bin = uint32_t(2 * tid + 1);
+          sh_above = acc;
+        } else if (acc + h1 < target && acc + h1 + h0 >= target) {
+          sh_bin = uint32_t(2 * tid);
+          sh_above = acc + h1;
+        }
+        __syncthreads();
+        prefix |= sh_bin << sh;
+        pmask |= dmask << sh;
+        above = sh_above;
+      }
+      bstar = prefix;
+      // ---- exact fp64 boundary (+ certification for Top-P)
+      double A = 0.0;
+      int gt = 0, E = 0;
+      for (int j = tid; j < n; j += kFusedThreads) {
+        const uint32_t x = __float_as_uint(sc[j]);
+        if (x > bstar) {
+          A += double(sc[j]);
+          ++gt;
+        }
+        if (x == bstar) ++E;
+      }
+      A = block_sum_f64(A, dsh);
+      gt = block_sum_i32(gt, ish);
+      E = block_sum_i32(E, ish);
+      E_sh = E;
+      if (topk) {
+        ties_needed = kk - gt;
+      } else {
+        if (tid == 0) {
+          const double T = sa.P * total;
+          const double eps = 4.0 * double(n) * 0x1p-53 * total;
+          const double vstar = double(__uint_as_float(bstar));
+          double c = A;
+          bool cert = (T - c) > eps;
+          int k = 0;
+          while (k < E) {
+            c += vstar;
+            ++k;
+            if (c >= T) break;
+            cert = cert && (T - c) > eps;
+          }
+          cert = cert && (c >= T) && (c - T) > eps;
+          sh_ties = k;
+          sh_cum = c;
+          sh_cert = cert ? 1 : 0;
+        }
+        __syncthreads();
+        ties_needed = sh_ties;
+        cum = sh_cum;
+        certified = sh_cert != 0;
+      }
+    }
+    if (!certified) {
+      // exact sorted walk (select_fallback_fused_kernel recomputes the row)
+      if (tid == 0) sa.fb_rows[atomicAdd(sa.fb_count, 1)] = int32_t(row);
+      __syncthreads();
+      continue;
+    }
+    // ---- emit: bits, counts, coverage, ascending indices. Ties of v* need ranks
+    // (ascending index) only when some but not all of them are taken.
+    const int nw = (n + 31) >> 5;  // words that can hold selected bits
+    const bool tie_ranks = mode == 0 && ties_needed > 0 && ties_needed < E_sh;
+    if (tie_ranks) {
+      for (int w = wid; w < nw; w += kFusedWarps) {
+        const int idx = w * 32 + lane;
+        const bool tie = idx < n && __float_as_uint(sc[idx]) == bstar;
+        const uint32_t tm = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) wcnt[w] = __popc(tm);
+      }
+      __syncthreads();
+      word_scan(wcnt, wpre, nw);
+      __syncthreads();
+    }
+    double smass = 0.0;
+    int cnt = 0;
+    for (int w = wid; w < W; w += kFusedWarps) {
+      const int idx = w * 32 + lane;
+      const bool valid = idx < n;
+      bool sel;
+      if (mode == 1) {
+        sel = valid;
+      } else if (mode == 2) {
+        sel = idx == n - 1;
+      } else {
+        const uint32_t x = valid ? __float_as_uint(sc[idx]) : 0u;
+        const bool tie = valid && x == bstar;
+        if (tie_ranks) {
+          const uint32_t tm = __ballot_sync(0xffffffffu, tie);
+          sel = valid && (x > bstar || (tie && wpre[w] + __popc(tm & lt_mask) < ties_needed));
+        } else {
+          sel = valid && (x > bstar || (tie && ties_needed > 0));
+        }
+      }
+      const uint32_t word = __ballot_sync(0xffffffffu, sel);
+      if (sel && topk) smass += double(sc[idx]);
+      cnt += __popc(word);
+      if (lane == 0) {
+        sa.mask_bits[row * W + w] = word;
+        if (w < nw) wbits[w] = word;
+      }
+    }
+    const int count = block_sum_i32(lane == 0 ? cnt : 0, ish);
+    if (sa.indices) {
+      if (tid < nw) wcnt[tid] = __popc(wbits[tid]);
+      __syncthreads();
+      word_scan(wcnt, wpre, nw);
+      __syncthreads();
+      for (int w = wid; w < nw; w += kFusedWarps) {
+        const uint32_t word = wbits[w];
+        if ((word >> lane) & 1u) sa.indices[row * N + wpre[w] + __popc(word & lt_mask)] = int16_t(w * 32 + lane);
+      }
+    }
+    const double m = topk ? block_sum_f64(smass, dsh) : 0.0;
+    if (tid == 0) {
+      double cov;
+      if (topk) cov = total > 0.0 ? m / total : 1.0;
+      else cov = mode == 0 ? cum / total : 1.0;
+      if (sa.counts) sa.counts[row] = count;
+      if (sa.coverage) sa.coverage[row] = cov;
+    }
+    __syncthreads();
+  }
+}
+
+// Exact reference walk for the fused path's uncertified rows: the row's scores are
+// recomputed from the partials (same arithmetic), then the sorted fp64 walk of
+// select_fallback_kernel.
+template <int SW, int RQ, int SPB>
+__global__ void __launch_bounds__(256) select_fallback_fused_kernel(const ProxyArgs pa, SelectArgs a) {
+  __shared__ unsigned long long keys[kFbMaxN];
+  __shared__ uint8_t flag[kFbMaxN];
+  __shared__ float lse_sh[64];
+  __shared__ int sh_k;
+  __shared__ double sh_cov;
+  const int count = *a.fb_count;
+  const int rq = RQ > 0 ? RQ : pa.rq;
+  for (int e = blockIdx.x; e < count; e += gridDim.x) {
+    const long long row = a.fb_rows[e];
+    const int plane = int(row / a.N), i = int(row % a.N), n = i + 1;
+    if (threadIdx.x < rq) lse_sh[threadIdx.x] = pa.lse2[(long long)plane * pa.Lq + (long long)i * rq + threadIdx.x];
+    __syncthreads();
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+      if (t < n) {
+        float f = proxy_block_score<SW, RQ, SPB>(pa, plane, i, t, lse_sh);
+        if (!(f >= 0.f) || f == 0.f) f = 0.f;
+        keys[t] = ((unsigned long long)(~__float_as_uint(f)) << 32) | unsigned(t);
+      } else {
+        keys[t] = ~0ull;
+      }
+      flag[t] = 0;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+          const int p = t ^ j;
+          if (p > t) {
+            const unsigned long long x = keys[t], y = keys[p];
+            const bool up = (t & k) == 0;
+            if ((x > y) == up) {
+              keys[t] = y;
+              keys[p] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    if (threadIdx.x == 0) {
+      auto val = [&](int t) { return double(__uint_as_float(~unsigned(keys[t] >> 32))); };
+      double total = 0.0;
+      for (int t = 0; t < n; ++t) total += val(t);
+      int ksel;
+      double cov = 1.0;
+      if (total <= 0.0) {
+        ksel = -1;
+      } else if (a.P >= 1.0) {
+        ksel = n;
+      } else {
+        double cum = 0.0;
+        ksel = 0;
+        for (int t = 0; t < n; ++t) {
+          ++ksel;
+          cum += val(t);
+          if (cum >= a.P * total) break;
+        }
+        cov = cum / total;
+      }
+      sh_k = ksel;
+      sh_cov = cov;
+    }
+    __syncthreads();
+    const int ksel = sh_k;
+    if (ksel < 0) {
+      if (threadIdx.x == 0) flag[n - 1] = 1;
+    } else {
+      for (int t = threadIdx.x; t < ksel; t += blockDim.x) flag[unsigned(keys[t] & 0xFFFFFFFFu)] = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int base = 0;
+      for (int w = 0; w < a.W; ++w) {
+        const int idx = w * 32 + lane;
+        const bool sel = idx < n && flag[idx];
+        const uint32_t word = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) a.mask_bits[row * a.W + w] = word;
+        if (a.indices && sel) a.indices[row * a.N + base + __popc(word & ((1u << lane) - 1u))] = int16_t(idx);
+        base += __popc(word);
+      }
+      if (lane == 0) {
+        if (a.counts) a.counts[row] = base;
+        if (a.coverage) a.coverage[row] = sh_cov;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int SW, int RQ, int SPB>
+void launch_fused_t(const ProxyArgs& pa, const SelectArgs& sa, cudaStream_t st) {
+  const int smem = sa.N * 4 + kRadixBins * 4;  // <= 24 KB (no attribute needed)
+  long long blocks = sa.rows;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  select_fused_kernel<SW, RQ, SPB><<<unsigned(blocks), kFusedThreads, smem, st>>>(pa, sa);
+  if (sa.select_mode == US_SELECT_TOP_P) select_fallback_fused_kernel<SW, RQ, SPB><<<148, 256, 0, st>>>(pa, sa);
+}
+
 __global__ void mask_check_kernel(const uint32_t* mask, int rows, int N, int W, uint32_t* err,
                                   int32_t* first_bad) {
   const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -371,6 +778,21 @@ us_status launch_select(const SelectArgs& a, cudaStream_t st) {
     select_fallback_kernel<<<148, 256, 0, st>>>(a);
     US_LAUNCH_CHECK("select_fallback_kernel");
   }
+  return US_OK;
+}
+
+us_status launch_select_fused(const ProxyArgs& pa, const SelectArgs& sa, cudaStream_t st) {
+  if (sa.N > kFbMaxN) {
+    set_error("select: N (=L/S) above 4096 is not supported on the GPU path");
+    return US_ERR_UNSUPPORTED;
+  }
+  if (pa.sw == 8 && pa.rq == 8 && pa.rk == 8) launch_fused_t<8, 8, 1>(pa, sa, st);
+  else if (pa.sw == 8) launch_fused_t<8, 0, 0>(pa, sa, st);
+  else if (pa.sw == 4) launch_fused_t<4, 0, 0>(pa, sa, st);
+  else if (pa.sw == 2) launch_fused_t<2, 0, 0>(pa, sa, st);
+  else launch_fused_t<1, 0, 0>(pa, sa, st);
+  US_LAUNCH_CHECK("select_fused_kernel");
+  if (sa.select_mode == US_SELECT_TOP_P) US_LAUNCH_CHECK("select_fallback_fused_kernel");
   return US_OK;
 }
 
