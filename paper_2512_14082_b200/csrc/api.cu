@@ -179,13 +179,13 @@ Ws layout(const us_params& p, bool scores_region = false) {
   w.absmax_q = take(4 * qplanes);
   w.absmax_k = take(4 * kplanes);
   w.header_bytes = o;
-  w.exp_q = take(4 * qplanes);
+  w.exp_q = take(4 * qplanes * g.Lq);  // one scale exponent per composite query row
   w.exp_k = take(4 * kplanes);
   const size_t rows = qplanes * g.N;
   w.fb_rows = take(4 * rows);
   // +128 rows of padding keep every TMA box inside the allocation
   const size_t qrows = qplanes * g.Lq + 128, krows = kplanes * g.Lk + 128;
-  w.qc = take(4 * qrows * g.D);
+  w.qc = 0;  // (Q is pooled straight into its fp16 hi/lo pair: no f32 copy in the workspace)
   w.kc = take(4 * krows * g.D);
   w.qh = take(2 * qrows * g.D);
   w.ql = take(2 * qrows * g.D);
@@ -224,17 +224,17 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   Geo g(p);
   Ws w = layout(p);
   US_CUDA_TRY(cudaMemsetAsync(ws, 0, w.header_bytes, st), "workspace clear");
+  // Q: pooling fused with the fp16 hi/lo split at a per-row power-of-two scale
+  // (compress.cu); K: f32 + per-plane |max|, then the split (K is 4-8x smaller)
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p.c_q, g.Hc, p.c_h, 1,
-                  at<float>(ws, w.qc), at<uint32_t>(ws, w.absmax_q), p.strategy, 0, p.seed, p.head0};
+                  nullptr, nullptr, p.strategy, 0, p.seed, p.head0,
+                  at<__half>(ws, w.qh), at<__half>(ws, w.ql), at<int>(ws, w.exp_q)};
   us_status s = launch_compress(cq, st);
   if (s != US_OK) return s;
   CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p.c_k, g.kv_planes,
                   g.kv_dedup ? 1 : p.c_h, g.kv_dedup ? 1 : g.G, at<float>(ws, w.kc),
                   at<uint32_t>(ws, w.absmax_k), p.strategy, 1, p.seed, p.head0};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
-  SplitArgs sq{at<float>(ws, w.qc), g.B * g.Hc, g.Lq, g.D, at<uint32_t>(ws, w.absmax_q),
-               at<int>(ws, w.exp_q), at<__half>(ws, w.qh), at<__half>(ws, w.ql)};
-  if ((s = launch_split(sq, st)) != US_OK) return s;
   SplitArgs sk{at<float>(ws, w.kc), g.B * g.kv_planes, g.Lk, g.D, at<uint32_t>(ws, w.absmax_k),
                at<int>(ws, w.exp_k), at<__half>(ws, w.kh), at<__half>(ws, w.kl)};
   if ((s = launch_split(sk, st)) != US_OK) return s;
@@ -260,6 +260,7 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   pa.kv_mul = g.kv_mul;
   pa.kv_div = g.kv_div;
   pa.exp_q = at<int>(ws, w.exp_q);
+  pa.q_row_exp = 1;
   pa.exp_k = at<int>(ws, w.exp_k);
   pa.qh = at<__half>(ws, w.qh);
   pa.ql = at<__half>(ws, w.ql);

@@ -63,7 +63,7 @@ __device__ __forceinline__ double group_sum(double v, int width) {
 // STRAT: the pooling strategy, compile-time so the mean kernel (the default path)
 // carries no registers for the max / stochastic code.
 template <int STRAT>
-__global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
+__global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
   const int chunks = a.d / 8;
   const int Lc = a.L / a.c;
   const long long total = (long long)a.B * a.planes * Lc * chunks;
@@ -202,10 +202,52 @@ __global__ void __launch_bounds__(256) compress_kernel(CompressArgs a, double in
 #pragma unroll
       for (int e = 0; e < 8; ++e) res[e] = __double2float_rn(divide(hacc[e], double(a.members), inv_m));
     }
-    if (active) {
+    if (active && a.out) {
       float4* dst = reinterpret_cast<float4*>(a.out + (((long long)plane_id) * Lc + t) * a.d + ch * 8);
       dst[0] = make_float4(res[0], res[1], res[2], res[3]);
       dst[1] = make_float4(res[4], res[5], res[6], res[7]);
+    }
+    if (a.hi) {
+      // fused split with a per-ROW power-of-two scale: the `chunks` lanes of the row
+      // reduce its |max| (as f32 bits; NaN stays above everything), then each lane
+      // writes x 2^e = hi + lo (fp16 pair, ~22 significant bits) for its 8 elements;
+      // e makes the row's |max| * 2^e land in [2^14, 2^15) (the split_kernel rule per row)
+      uint32_t mb = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float av = fabsf(res[e]);
+        mb = max(mb, av != av ? 0x7FC00000u : __float_as_uint(av));
+      }
+      for (int o = chunks >> 1; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o, chunks));
+      const float amax = __uint_as_float(mb);
+      int ex2 = 0;
+      if (amax > 0.f && amax < INFINITY) {
+        int ex;
+        frexpf(amax, &ex);
+        ex2 = 15 - ex;
+      }
+      __half h[8], l[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x = ldexpf(res[e], ex2);
+        h[e] = __float2half_rn(x);
+        l[e] = __float2half_rn(x - __half2float(h[e]));
+      }
+      if (active) {
+        const long long o = (((long long)plane_id) * Lc + t) * a.d + ch * 8;
+        uint4 hv, lv;
+        hv.x = uint32_t(__half_as_ushort(h[0])) | (uint32_t(__half_as_ushort(h[1])) << 16);
+        hv.y = uint32_t(__half_as_ushort(h[2])) | (uint32_t(__half_as_ushort(h[3])) << 16);
+        hv.z = uint32_t(__half_as_ushort(h[4])) | (uint32_t(__half_as_ushort(h[5])) << 16);
+        hv.w = uint32_t(__half_as_ushort(h[6])) | (uint32_t(__half_as_ushort(h[7])) << 16);
+        lv.x = uint32_t(__half_as_ushort(l[0])) | (uint32_t(__half_as_ushort(l[1])) << 16);
+        lv.y = uint32_t(__half_as_ushort(l[2])) | (uint32_t(__half_as_ushort(l[3])) << 16);
+        lv.z = uint32_t(__half_as_ushort(l[4])) | (uint32_t(__half_as_ushort(l[5])) << 16);
+        lv.w = uint32_t(__half_as_ushort(l[6])) | (uint32_t(__half_as_ushort(l[7])) << 16);
+        *reinterpret_cast<uint4*>(a.hi + o) = hv;
+        *reinterpret_cast<uint4*>(a.lo + o) = lv;
+        if (ch == 0) a.row_exp[(long long)plane_id * Lc + t] = ex2;
+      }
     }
   }
   if (a.absmax) {

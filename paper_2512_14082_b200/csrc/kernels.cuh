@@ -31,6 +31,10 @@ struct CompressArgs {
   int role;        // stochastic seed tag: 0 = Q, 1 = K (compression.cpp:17-20)
   uint64_t seed;   // CompressionConfig::seed
   int head0;       // global index of the call's first head (stochastic seeds use head0 + h)
+  // fused split (nullable): fp16 hi/lo of out * 2^row_exp[row] per output row [B*planes][L/c][d]
+  __half* hi;
+  __half* lo;
+  int* row_exp;    // [B*planes][L/c]
 };
 us_status launch_compress(const CompressArgs& a, cudaStream_t st);
 
@@ -54,7 +58,7 @@ struct ProxyArgs {
   int causal_mode;
   int kv_planes;       // K planes per batch item
   int kv_mul, kv_div;  // K plane of compressed head hc = hc * kv_mul / kv_div
-  const int* exp_q;    // [B*Hc]
+  const int* exp_q;    // [B*Hc][Lq] per composite row (q_row_exp = 1) or [B*Hc] per plane
   const int* exp_k;    // [B*kv_planes]
   const __half* qh;    // [B*Hc][Lq][D] fp16 hi of Qc * 2^e
   const __half* ql;    // [B*Hc][Lq][D] fp16 lo
@@ -73,6 +77,7 @@ struct ProxyArgs {
   int k_phase;         // key phase class (3-D K map: (d, stride, rows/stride))
   int live_bias;       // live keys of composite row r = r + live_bias
   int accumulate;      // finalize adds into scores instead of overwriting
+  int q_row_exp;       // 1: exp_q holds one exponent per composite query row
   int finalize;        // 1: launch the finalize (block scores into `scores`); 0: the caller
                        //    fuses it into the selection (launch_select_fused)
 };

@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(320, 1)
     const int live = !row_ok ? 0
                      : X3    ? live_keys(t_row, a.c_q, a.c_k, a.Lk, a.causal_mode)
                              : max(0, min(a.Lk, t_row + a.live_bias));
-    const float k2 = X3 ? ldexpf(a.scale_log2, -(a.exp_q[plane] + a.exp_k[kplane])) : a.scale_log2;
+    const int eq = !X3 ? 0 : (a.q_row_exp ? (row_ok ? a.exp_q[(long long)plane * a.Lq + t_row] : 0) : a.exp_q[plane]);
+    const float k2 = X3 ? ldexpf(a.scale_log2, -(eq + a.exp_k[kplane])) : a.scale_log2;
     float m = -INFINITY, l = 0.f;
     for (int t = grp; t < n_tiles; t += 2) {
       mbar_wait(&bar_sfull[grp], (t >> 1) & 1);
