@@ -66,9 +66,11 @@ struct AttentionInputs {
   int L = 0;
   int d_k = 0;
   int S = 64;
-  const void* Q = nullptr;  // bf16 [B][H][L][d_k]
+  const void* Q = nullptr;  // bf16 [B][H][L][d_k] (f32 when f32 = true)
   const void* K = nullptr;  // bf16 [B][H_kv][L][d_k]
   const void* V = nullptr;  // bf16 [B][H_kv][L][d_k]
+  bool f32 = false;         // Q/K/V hold f32 (the reference HeadStack<float> storage):
+                            // pooled as f32 (fp64 sums); attention runs on bf16 copies
   cudaStream_t stream = nullptr;
 };
 
@@ -187,6 +189,7 @@ inline us_params params(const AttentionInputs& in, const CompressionConfig& cfg,
   p.top_k = cfg.top_k;
   p.flags = sync_check ? US_FLAG_SYNC_CHECK : 0;
   p.seed = cfg.seed;
+  p.dtype = in.f32 ? US_DTYPE_F32 : US_DTYPE_BF16;
   return p;
 }
 
@@ -372,7 +375,10 @@ inline AttentionOutput dense_attention(const AttentionInputs& in) {
   AttentionOutput out;
   out.O = DeviceBuffer<std::uint16_t>(size_t(in.B) * in.H * in.L * in.d_k);
   out.lse = DeviceBuffer<float>(size_t(in.B) * in.H * in.L);
-  detail::raise(us_dense_attention(&p, in.Q, in.K, in.V, out.O.data(), out.lse.data(), nullptr, 0, in.stream));
+  DeviceBuffer<std::uint8_t> ws;  // f32 inputs: the bf16 copies live in the workspace
+  if (in.f32) ws = detail::workspace(p);
+  detail::raise(us_dense_attention(&p, in.Q, in.K, in.V, out.O.data(), out.lse.data(), ws.data(), ws.size(),
+                                   in.stream));
   return out;
 }
 

@@ -19,7 +19,7 @@
  * Conventions
  *   * Tensors are device pointers, head-major (the reference HeadStack order,
  *     tensor_io.hpp:9-11) with a leading batch dim:
- *       Q, O      bf16 [B][H][L][d_k]
+ *       Q, O      bf16 [B][H][L][d_k]   (Q / K / V f32 when params.dtype = US_DTYPE_F32)
  *       K, V      bf16 [B][H_kv][L][d_k]   (GQA: head h reads KV head h/(H/H_kv);
  *                                          H_kv == H is the reference layout)
  *       lse       f32  [B][H][L]           natural log, reference AttentionOutput::lse
@@ -68,6 +68,8 @@ enum { US_POST_SOFTMAX_BLOCK_CAUSAL = 0, US_PRE_SOFTMAX_COMPRESSED_CAUSAL = 1 };
 enum { US_SELECT_TOP_P = 0, US_SELECT_TOP_K = 1 };
 /* ProxyTag (types.hpp:45) for us_selection_flops */
 enum { US_PROXY_UNISPARSE = 0, US_PROXY_ANTIDIAGONAL = 1, US_PROXY_LAST_BLOCK = 2 };
+/* params.dtype */
+enum { US_DTYPE_BF16 = 0, US_DTYPE_F32 = 1 };
 /* params.flags */
 enum { US_FLAG_SYNC_CHECK = 1 };
 
@@ -88,6 +90,11 @@ typedef struct us_params {
   int32_t top_k;       /* k for US_SELECT_TOP_K */
   int32_t flags;       /* US_FLAG_* */
   uint64_t seed;       /* stochastic pooling seed (unused by Mean) */
+  int32_t dtype;       /* US_DTYPE_BF16 (0, default) or US_DTYPE_F32: storage of Q, K, V.
+                          F32 is the reference's own HeadStack<float> (types.hpp:15-26):
+                          compress / select pool the f32 values (fp64 window sums,
+                          compression.hpp:26-28); attention computes on bf16 copies made
+                          in the workspace (O stays bf16). */
   int32_t head0;       /* global index of this call's first Q head (0 for a whole layer): a
                           call on a head range [head0, head0 + H) of a larger layer (head
                           sharding, chunked pipelines) seeds stochastic pooling with the

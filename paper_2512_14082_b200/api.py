@@ -35,6 +35,7 @@ US_OK, US_ERR_INVALID_ARGUMENT, US_ERR_UNSUPPORTED, US_ERR_CUDA, US_ERR_INVALID_
     US_ERR_NONFINITE, US_ERR_WORKSPACE, US_ERR_IO = range(8)
 POOL_MEAN, POOL_MAX, POOL_STOCHASTIC = 0, 1, 2
 POST_SOFTMAX_BLOCK_CAUSAL, PRE_SOFTMAX_COMPRESSED_CAUSAL = 0, 1
+DTYPE_BF16, DTYPE_F32 = 0, 1
 SELECT_TOP_P, SELECT_TOP_K = 0, 1
 PROXY_UNISPARSE, PROXY_ANTIDIAGONAL, PROXY_LAST_BLOCK = 0, 1, 2
 FLAG_SYNC_CHECK = 1
@@ -61,7 +62,7 @@ class UsParams(C.Structure):
                 ("d_k", C.c_int32), ("S", C.c_int32), ("c_q", C.c_int32), ("c_k", C.c_int32),
                 ("c_h", C.c_int32), ("strategy", C.c_int32), ("causal_mode", C.c_int32),
                 ("select_mode", C.c_int32), ("P", C.c_double), ("top_k", C.c_int32),
-                ("flags", C.c_int32), ("seed", C.c_uint64), ("head0", C.c_int32)]
+                ("flags", C.c_int32), ("seed", C.c_uint64), ("dtype", C.c_int32), ("head0", C.c_int32)]
 
 
 class UsSelection(C.Structure):
@@ -164,9 +165,10 @@ def make_params(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int
     layer (head sharding): stochastic pooling seeds with the global head index."""
     B, H, L, d = _bhld(Q)
     H_kv = _bhld(K)[1]
+    dtype = DTYPE_F32 if Q.dtype == torch.float32 else DTYPE_BF16
     return UsParams(B, H, H_kv, L, d, S, cfg.c_q, cfg.c_k, cfg.c_h, cfg.strategy, cfg.causal_mode,
                     cfg.select_mode, float(cfg.P), cfg.top_k, FLAG_SYNC_CHECK if sync_check else 0,
-                    cfg.seed, head0)
+                    cfg.seed, dtype, head0)
 
 
 def _bhld(x: torch.Tensor):
@@ -199,8 +201,10 @@ def _check_inputs(*ts: torch.Tensor):
             dev = t.device
         if not t.is_cuda:
             raise ValueError("inputs must be CUDA tensors (the GPU path has no CPU fallback)")
-        if t.dtype != torch.bfloat16:
-            raise ValueError(f"inputs must be bfloat16, got {t.dtype}")
+        if t.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"inputs must be bfloat16 or float32, got {t.dtype}")
+        if t.dtype != ts[0].dtype:
+            raise ValueError(f"inputs must share one dtype ({ts[0].dtype} and {t.dtype})")
         if not t.is_contiguous():
             raise ValueError("inputs must be contiguous")
 
@@ -375,10 +379,10 @@ def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: in
     """block_sparse_attention (attention.cpp:89-137). mask_bits: int32 [B, planes, N, W]."""
     _check_inputs(Q, K, V)
     p = make_params(Q, K, CompressionConfig(c_q=1, c_k=1, c_h=1), S, validate_mask)
-    O = torch.empty_like(Q)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
-    ws = workspace(p) if validate_mask else None
+    ws = workspace(p) if (validate_mask or Q.dtype == torch.float32) else None
     _raise(lib().us_sparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(mask_bits.contiguous()),
                                      heads_per_plane, _ptr(O), _ptr(lse), _ptr(ws),
                                      ws.numel() if ws is not None else 0, _stream()))
@@ -394,7 +398,7 @@ def unisparse_attn(Q, K, V, cfg: CompressionConfig, S: int = 64, with_scores: bo
     ws = workspace(p)
     sel = _alloc_selection(p, with_scores, with_indices)
     ss = _sel_struct(sel)
-    O = torch.empty_like(Q)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device)
     _raise(lib().us_unisparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse),
@@ -407,11 +411,12 @@ def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True):
     """Causal dense attention via the same kernel with every causal block selected."""
     _check_inputs(Q, K, V)
     p = make_params(Q, K, CompressionConfig(c_q=1, c_k=1, c_h=1), S)
-    O = torch.empty_like(Q)
+    O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
-    _raise(lib().us_dense_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse), None, 0,
-                                    _stream()))
+    ws = workspace(p) if Q.dtype == torch.float32 else None  # f32 inputs: bf16 copies in the workspace
+    _raise(lib().us_dense_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse), _ptr(ws),
+                                    ws.numel() if ws is not None else 0, _stream()))
     return O, lse
 
 
@@ -429,7 +434,7 @@ class Engine:
                               device=Q.device)
         self.sel = _alloc_selection(self.p, False, False)
         self.ss = _sel_struct(self.sel)
-        self.O = torch.empty_like(Q)
+        self.O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
         B, H, L, _ = _bhld(Q)
         self.lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device)
         self.Q, self.K, self.V = Q, K, V
@@ -441,7 +446,8 @@ class Engine:
     def _run(self, dense: bool = False):
         if dense:
             _raise(lib().us_dense_attention(C.byref(self.p), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
-                                            _ptr(self.O), _ptr(self.lse), None, 0, _stream()))
+                                            _ptr(self.O), _ptr(self.lse), _ptr(self.ws), self.ws.numel(),
+                                            _stream()))
         else:
             _raise(lib().us_unisparse_attention(C.byref(self.p), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
                                                 _ptr(self.O), _ptr(self.lse), C.byref(self.ss),
@@ -468,7 +474,7 @@ class Engine:
         for n in sizes:
             q0, q1 = kv0 * G, (kv0 + n) * G
             cp = UsParams(1, n * G, n, p.L, p.d_k, p.S, p.c_q, p.c_k, p.c_h, p.strategy, p.causal_mode,
-                          p.select_mode, p.P, p.top_k, p.flags, p.seed, p.head0 + q0)
+                          p.select_mode, p.P, p.top_k, p.flags, p.seed, p.dtype, p.head0 + q0)
             pl0, pl1 = q0 // p.c_h, q1 // p.c_h
             sel = UsSelection(self.sel.mask_bits[0, pl0:pl1].data_ptr(), self.sel.counts[0, pl0:pl1].data_ptr(),
                               self.sel.coverage[0, pl0:pl1].data_ptr(), None, None)

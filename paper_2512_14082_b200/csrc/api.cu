@@ -78,6 +78,7 @@ Checked check(const us_params& p, bool need_compression) {
     e.push_back("H=" + std::to_string(p.H) + " not divisible by H_kv=" + std::to_string(p.H_kv));
   if (p.B <= 0) e.push_back("B must be positive");
   if (p.head0 < 0) e.push_back("head0 must be non-negative");
+  if (p.dtype != US_DTYPE_BF16 && p.dtype != US_DTYPE_F32) e.push_back("unknown dtype");
   if (p.select_mode != US_SELECT_TOP_P && p.select_mode != US_SELECT_TOP_K)
     e.push_back("unknown select_mode");
   if (p.select_mode == US_SELECT_TOP_K && p.top_k < 1) e.push_back("top_k must be positive");
@@ -154,7 +155,7 @@ struct Geo {
 
 struct Ws {
   size_t err, first_bad, fb_count, absmax_q, absmax_k, exp_q, exp_k, fb_rows, qc, kc, qh, ql, kh,
-      kl, lse2, part, tmax, scores, mask, total;
+      kl, lse2, part, tmax, scores, mask, conv, total;
   size_t header_bytes;  // [0, header_bytes) is cleared before each selection
 };
 
@@ -199,6 +200,8 @@ Ws layout(const us_params& p, bool scores_region = false) {
   w.tmax = take(4 * qplanes * T * g.Lq);
   w.scores = scores_region ? take(4 * rows * g.N) : 0;
   w.mask = take(4 * rows * g.W);
+  // f32 inputs: bf16 copies of Q, K, V for the attention kernels
+  w.conv = p.dtype == US_DTYPE_F32 ? take(2 * (size_t(g.B) * g.H + 2 * size_t(g.B) * g.H_kv) * g.L * g.D) : 0;
   w.total = o;
   return w;
 }
@@ -228,12 +231,13 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   // (compress.cu); K: f32 + per-plane |max|, then the split (K is 4-8x smaller)
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p.c_q, g.Hc, p.c_h, 1,
                   nullptr, nullptr, p.strategy, 0, p.seed, p.head0,
-                  at<__half>(ws, w.qh), at<__half>(ws, w.ql), at<int>(ws, w.exp_q)};
+                  at<__half>(ws, w.qh), at<__half>(ws, w.ql), at<int>(ws, w.exp_q), p.dtype == US_DTYPE_F32};
   us_status s = launch_compress(cq, st);
   if (s != US_OK) return s;
   CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p.c_k, g.kv_planes,
                   g.kv_dedup ? 1 : p.c_h, g.kv_dedup ? 1 : g.G, at<float>(ws, w.kc),
-                  at<uint32_t>(ws, w.absmax_k), p.strategy, 1, p.seed, p.head0};
+                  at<uint32_t>(ws, w.absmax_k), p.strategy, 1, p.seed, p.head0,
+                  nullptr, nullptr, nullptr, p.dtype == US_DTYPE_F32};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
   SplitArgs sk{at<float>(ws, w.kc), g.B * g.kv_planes, g.Lk, g.D, at<uint32_t>(ws, w.absmax_k),
                at<int>(ws, w.exp_k), at<__half>(ws, w.kh), at<__half>(ws, w.kl)};
@@ -433,8 +437,29 @@ int attention_pairing() {
 
 us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
                         const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st,
-                        uint32_t* err = nullptr, int32_t* first_bad = nullptr) {
+                        uint32_t* err = nullptr, int32_t* first_bad = nullptr, void* ws = nullptr) {
   Geo g(p);
+  if (p.dtype == US_DTYPE_F32) {
+    // the attention kernels compute on bf16 copies of f32 inputs (round to nearest even)
+    if (!ws) {
+      set_error("attention: f32 inputs need the workspace (us_workspace_bytes) for their bf16 copies");
+      return US_ERR_WORKSPACE;
+    }
+    Ws w = layout(p);
+    uint8_t* qb = at<uint8_t>(ws, w.conv);
+    uint8_t* kb = qb + size_t(2) * g.B * g.H * g.L * g.D;
+    uint8_t* vb = kb + size_t(2) * g.B * g.H_kv * g.L * g.D;
+    us_status s;
+    if ((s = launch_f32_to_bf16(static_cast<const float*>(Q), qb, (long long)g.B * g.H * g.L * g.D, st)) != US_OK)
+      return s;
+    if ((s = launch_f32_to_bf16(static_cast<const float*>(K), kb, (long long)g.B * g.H_kv * g.L * g.D, st)) != US_OK)
+      return s;
+    if ((s = launch_f32_to_bf16(static_cast<const float*>(V), vb, (long long)g.B * g.H_kv * g.L * g.D, st)) != US_OK)
+      return s;
+    us_params pb = p;
+    pb.dtype = US_DTYPE_BF16;
+    return run_attention(pb, qb, kb, vb, mask, hpp, O, lse, st, err, first_bad, nullptr);
+  }
   CUtensorMap tQ, tK, tV;
   us_status s;
   if ((s = make_tmap_2d_16b(&tQ, Q, uint64_t(g.B) * g.H * g.L, g.D, 64, 64, true)) != US_OK) return s;
@@ -586,10 +611,10 @@ us_status us_compress(const us_params* p, const void* Q, const void* K, float* Q
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // reference layout: H/c_h planes for both Q and K (K expanded to H heads first)
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p->c_q, g.Hc, p->c_h, 1, Qc, nullptr,
-                  p->strategy, 0, p->seed, p->head0};
+                  p->strategy, 0, p->seed, p->head0, nullptr, nullptr, nullptr, p->dtype == US_DTYPE_F32};
   if ((s = launch_compress(cq, st)) != US_OK) return s;
   CompressArgs ck{static_cast<const uint16_t*>(K), g.B, g.H_kv, g.L, g.D, p->c_k, g.Hc, p->c_h, g.G, Kc, nullptr,
-                  p->strategy, 1, p->seed, p->head0};
+                  p->strategy, 1, p->seed, p->head0, nullptr, nullptr, nullptr, p->dtype == US_DTYPE_F32};
   if ((s = launch_compress(ck, st)) != US_OK) return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "compress");
   return US_OK;
@@ -886,7 +911,21 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
       return s;
     if ((s = sync_check(*p, workspace, st, "block_sparse_attention")) != US_OK) return s;
   }
-  if ((s = run_attention(*p, Q, K, V, mask_bits, heads_per_plane, O, lse, st)) != US_OK) return s;
+  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK)
+    return s;
+  uint32_t* err = nullptr;
+  int32_t* first_bad = nullptr;
+  if (workspace && workspace_bytes >= layout(*p).total) {
+    // asynchronous data-error report (us_check_device_errors): the kernel ORs 4 (a
+    // non-causal bit) or 8 (an empty row) into the sticky error word and records the
+    // first offending row, as the reference throws (attention.cpp:106-108, 127-129)
+    Ws w = layout(*p);
+    err = at<uint32_t>(workspace, w.err);
+    first_bad = at<int32_t>(workspace, w.first_bad);
+    US_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7F, 4, st), "workspace clear");
+  }
+  if ((s = run_attention(*p, Q, K, V, mask_bits, heads_per_plane, O, lse, st, err, first_bad, workspace)) != US_OK)
+    return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "block_sparse_attention");
   return US_OK;
 }
@@ -909,7 +948,7 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
   uint32_t* mask = (sel && sel->mask_bits) ? sel->mask_bits : at<uint32_t>(workspace, w.mask);
   if ((s = run_select_fused(*p, pa, mask, sel, workspace, st)) != US_OK) return s;
   g_prof.mark(call, 3, st);
-  if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st)) != US_OK) return s;
+  if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st, nullptr, nullptr, workspace)) != US_OK) return s;
   g_prof.mark(call, 4, st);
   if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "unisparse_attn");
   return US_OK;
@@ -918,12 +957,11 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
 us_status us_dense_attention(const us_params* p, const void* Q, const void* K, const void* V,
                              void* O, float* lse, void* workspace, size_t workspace_bytes,
                              void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
   us_status s = gate(p, "dense_attention", false);
   if (s != US_OK) return s;
+  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "dense_attention")) != US_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((s = run_attention(*p, Q, K, V, nullptr, 1, O, lse, st)) != US_OK) return s;
+  if ((s = run_attention(*p, Q, K, V, nullptr, 1, O, lse, st, nullptr, nullptr, workspace)) != US_OK) return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "dense_attention");
   return US_OK;
 }

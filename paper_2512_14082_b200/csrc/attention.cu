@@ -274,6 +274,31 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       }
     }
     __syncwarp();
+    if (a.err && a.mask) {
+      // asynchronous data-error report (the reference throws, attention.cpp:106-108,
+      // 127-129): a non-causal bit anywhere in a group's row, or an empty causal prefix
+      for (int g = 0; g < 4; ++g) {
+        if (!gr.en[g]) continue;
+        const int ig = gr.i[g];
+        const long long row = (long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + ig;
+        const uint32_t* src = a.mask + row * a.W;
+        uint32_t bad = 0;
+        int cnt = 0;
+        for (int w = lane; w < a.W; w += 32) {
+          const uint32_t word = src[w];
+          const int lo = w << 5;
+          const uint32_t keep = lo > ig ? 0u : (ig - lo >= 31 ? ~0u : (2u << (ig - lo)) - 1u);
+          bad |= word & ~keep;
+          cnt += __popc(word & keep);
+        }
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0 && (bad || cnt == 0)) {
+          atomicOr(a.err, bad ? 4u : 8u);
+          atomicMin(a.first_bad, int32_t(row));
+        }
+      }
+    }
     // Pair the four groups into the two tiles so that the LONGER tile's step count
     // (its pair's union) is smallest: the CTA lasts as long as its longer tile, and
     // the per-head selection sizes differ (tools/tile_pairing.py: -11 % on the sum

@@ -37,6 +37,26 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
+// 8 consecutive input elements of row `row` (in units of rows of d elements) as f32:
+// bf16 storage (one 16-byte load) or f32 storage (two), both exact.
+template <bool F32>
+__device__ __forceinline__ void load8(const void* base, long long elem, float (&x)[8]) {
+  if (F32) {
+    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const float*>(base) + elem);
+    const uint4 a = ld_stream(p), b = ld_stream(p + 1);
+    x[0] = __uint_as_float(a.x); x[1] = __uint_as_float(a.y); x[2] = __uint_as_float(a.z); x[3] = __uint_as_float(a.w);
+    x[4] = __uint_as_float(b.x); x[5] = __uint_as_float(b.y); x[6] = __uint_as_float(b.z); x[7] = __uint_as_float(b.w);
+  } else {
+    const uint4 v = ld_stream(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + elem));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      x[2 * q] = __uint_as_float(w[q] << 16);
+      x[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+    }
+  }
+}
+
 // inv: exact reciprocal when the divisor is a power of two (then x*inv == x/div
 // bit for bit), else 0 and a true fp64 division is used.
 __device__ __forceinline__ double divide(double x, double div, double inv) {
@@ -62,7 +82,9 @@ __device__ __forceinline__ double group_sum(double v, int width) {
 
 // STRAT: the pooling strategy, compile-time so the mean kernel (the default path)
 // carries no registers for the max / stochastic code.
-template <int STRAT>
+// F32: f32 input storage (the reference's own HeadStack<float>, C1): every strategy
+// sums in fp64 in row order like the oracle; the bf16 fp32-exact fast path is skipped.
+template <int STRAT, bool F32>
 __global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
   const int chunks = a.d / 8;
   const int Lc = a.L / a.c;
@@ -86,12 +108,12 @@ __global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_k
     for (int g = 0; g < a.members; ++g) {
       const int h = p * a.members + g;  // head index in the reference's (expanded) numbering
       const int hs = h / a.div;
-      const uint4* src = reinterpret_cast<const uint4*>(
-          a.src + (((long long)b * a.H_src + hs) * a.L + (long long)t * a.c) * a.d + ch * 8);
-      const int stride = a.d / 8;  // uint4 per row
+      const long long elem0 = (((long long)b * a.H_src + hs) * a.L + (long long)t * a.c) * a.d + ch * 8;
+      const uint4* src = reinterpret_cast<const uint4*>(a.src + (F32 ? 0 : elem0));
+      const int stride = a.d / 8;  // uint4 per row (bf16)
       float val[8];
       bool done = false;
-      if (STRAT == US_POOL_MEAN && a.c > 1 && inv_c != 0.0) {
+      if (!F32 && STRAT == US_POOL_MEAN && a.c > 1 && inv_c != 0.0) {
         // fp32 fast path: the running sum (from +0, row order, round-to-nearest) is
         // kept only if every addition was exact (round-down == round-up), so it
         // equals the fp64 sum; times the exact 1/c it rounds like the fp64 path
@@ -130,7 +152,16 @@ __global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_k
         // (the fp64 path: c == 1, non-power-of-two c, or a window the fp32 path
         // could not sum exactly — rare, so one row in flight keeps registers low)
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int rr = 0; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
+        if (F32) {
+          for (int rr = 0; rr < a.c; ++rr) {
+            float x[8];
+            load8<true>(a.src, elem0 + (long long)rr * a.d, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += double(x[e]);
+          }
+        } else {
+          for (int rr = 0; rr < a.c; ++rr) bf16x8_to_f64_add(ld_stream(src + rr * stride), acc);
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) val[e] = __double2float_rn(divide(acc[e], double(a.c), inv_c));
       } else if (STRAT == US_POOL_MAX) {
@@ -138,13 +169,10 @@ __global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_k
 #pragma unroll
         for (int e = 0; e < 8; ++e) val[e] = -INFINITY;
         for (int rr = 0; rr < a.c; ++rr) {
-          const uint4 v = ld_stream(src + rr * stride);
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          float x[8];
+          load8<F32>(a.src, elem0 + (long long)rr * a.d, x);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            val[2 * q] = fmaxf(val[2 * q], __uint_as_float(w[q] << 16));
-            val[2 * q + 1] = fmaxf(val[2 * q + 1], __uint_as_float(w[q] & 0xFFFF0000u));
-          }
+          for (int e = 0; e < 8; ++e) val[e] = fmaxf(val[e], x[e]);
         }
       } else {
         // stochastic (compression.hpp:33-53): pick window row r with probability
@@ -152,15 +180,11 @@ __global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_k
         // Row norms: fp64 sums of squares (exact for bf16 inputs), sqrt, summed in row order.
         uint64_t state = chain_seed(chain_seed(chain_seed(a.seed, uint64_t(a.role)), uint64_t(a.head0 + h)), uint64_t(t));
         auto row_norm = [&](int rr) {
-          const uint4 v = ld_stream(src + rr * stride);
-          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          float x[8];
+          load8<F32>(a.src, elem0 + (long long)rr * a.d, x);
           double s2 = 0.0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double lo = double(__uint_as_float(w[q] << 16)), hi = double(__uint_as_float(w[q] & 0xFFFF0000u));
-            s2 += lo * lo;
-            s2 += hi * hi;
-          }
+          for (int e = 0; e < 8; ++e) s2 += double(x[e]) * double(x[e]);
           return sqrt(group_sum(s2, chunks));
         };
         double tot = 0.0;
@@ -182,13 +206,7 @@ __global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_k
         } else {
           pick = int(draw % uint64_t(a.c));
         }
-        const uint4 v = ld_stream(src + pick * stride);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          val[2 * q] = __uint_as_float(w[q] << 16);
-          val[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
-        }
+        load8<F32>(a.src, elem0 + (long long)pick * a.d, val);
       }
       if (a.members == 1) {
 #pragma unroll
@@ -307,6 +325,15 @@ __global__ void __launch_bounds__(256) split_kernel(SplitArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float4* __restrict__ in, uint2* __restrict__ out,
+                                                          long long n4) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += (long long)gridDim.x * blockDim.x) {
+    const float4 v = in[q];
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    out[q] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  }
+}
+
 double exact_inverse(int c) { return (c > 0 && (c & (c - 1)) == 0) ? 1.0 / double(c) : 0.0; }
 
 }  // namespace
@@ -315,14 +342,33 @@ us_status launch_compress(const CompressArgs& a, cudaStream_t st) {
   const long long total = (long long)a.B * a.planes * (a.L / a.c) * (a.d / 8);
   const int threads = 256;
   const long long blocks = (total + threads - 1) / threads;
-  if (a.strategy == US_POOL_MAX)
-    compress_kernel<US_POOL_MAX><<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
-  else if (a.strategy == US_POOL_STOCHASTIC)
-    compress_kernel<US_POOL_STOCHASTIC>
-        <<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
-  else
-    compress_kernel<US_POOL_MEAN><<<unsigned(blocks), threads, 0, st>>>(a, exact_inverse(a.c), exact_inverse(a.members));
+  const double ic = exact_inverse(a.c), im = exact_inverse(a.members);
+  const unsigned g = unsigned(blocks);
+  if (a.src_f32) {
+    if (a.strategy == US_POOL_MAX) compress_kernel<US_POOL_MAX, true><<<g, threads, 0, st>>>(a, ic, im);
+    else if (a.strategy == US_POOL_STOCHASTIC) compress_kernel<US_POOL_STOCHASTIC, true><<<g, threads, 0, st>>>(a, ic, im);
+    else compress_kernel<US_POOL_MEAN, true><<<g, threads, 0, st>>>(a, ic, im);
+  } else {
+    if (a.strategy == US_POOL_MAX) compress_kernel<US_POOL_MAX, false><<<g, threads, 0, st>>>(a, ic, im);
+    else if (a.strategy == US_POOL_STOCHASTIC) compress_kernel<US_POOL_STOCHASTIC, false><<<g, threads, 0, st>>>(a, ic, im);
+    else compress_kernel<US_POOL_MEAN, false><<<g, threads, 0, st>>>(a, ic, im);
+  }
   US_LAUNCH_CHECK("compress_kernel");
+  return US_OK;
+}
+
+us_status launch_f32_to_bf16(const float* in, void* out, long long n, cudaStream_t st) {
+  if (n % 4) {
+    set_error("f32 -> bf16 conversion: element count must be a multiple of 4");
+    return US_ERR_UNSUPPORTED;
+  }
+  const long long n4 = n / 4;
+  long long blocks = (n4 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (n4 > 0)
+    f32_to_bf16_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(in),
+                                                          static_cast<uint2*>(out), n4);
+  US_LAUNCH_CHECK("f32_to_bf16_kernel");
   return US_OK;
 }
 

@@ -19,7 +19,7 @@ namespace us {
 // one f32 rounding per stage. Source head of member g of plane p is
 // (p * members + g) / div.
 struct CompressArgs {
-  const uint16_t* src;  // bf16 [B][H_src][L][d]
+  const uint16_t* src;  // bf16 [B][H_src][L][d] (f32 when src_f32; reinterpreted)
   int B, H_src, L, d;
   int c;           // window (c_q or c_k)
   int planes;      // output planes per batch item
@@ -35,6 +35,7 @@ struct CompressArgs {
   __half* hi;
   __half* lo;
   int* row_exp;    // [B*planes][L/c]
+  int src_f32;     // 1: src holds f32 values (the reference's fp32 HeadStack storage)
 };
 us_status launch_compress(const CompressArgs& a, cudaStream_t st);
 
@@ -49,6 +50,9 @@ struct SplitArgs {
   __half* lo;
 };
 us_status launch_split(const SplitArgs& a, cudaStream_t st);
+// f32 -> bf16 (round to nearest even) of n elements (n % 4 == 0): the bf16 copies
+// attention computes on when the caller's Q/K/V are f32 (us_params.dtype).
+us_status launch_f32_to_bf16(const float* in, void* out, long long n, cudaStream_t st);
 
 // ---------------------------------------------------------------- proxy (a2-a3)
 struct ProxyArgs {
