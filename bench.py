@@ -278,6 +278,52 @@ def _self_launch(n: int) -> int:
     return subprocess.run(cmd).returncode
 
 
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_c1_layer(repeats=3):
+    """BASELINE.md §3.2 CPU protocol: the reference's CPU path (oracle restatement,
+    fp64 on f32 storage) on the WHOLE C1 layer (Llama-3-8B shape 32 Q / 8 KV heads,
+    L = 4096, d = 128, S = 64, c = 8, Top-P 0.95, planted gain 8, fp32), per stage,
+    best of `repeats`, on 1 thread (the reference hot path is single-threaded) and on
+    all host threads (OpenMP over heads). Test infrastructure only."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_py as O
+    L, H, H_kv, d, S, P = 4096, 32, 8, 128, 64, 0.95
+    Q, K, V, _ = O.gen_workload(O.WL_PLANTED, L, H, d, S, 2512, H_kv=H_kv, gain=8.0)
+    c = O.cfg(H, L, d, S, H_kv=H_kv, P=P)
+    out = {"config": "C1: 32 Q / 8 KV heads, L=4096, d=128, S=64, c=8, Top-P 0.95, fp32 planted gain 8",
+           "cpu_model": _cpu_model(), "nproc": os.cpu_count()}
+    for label, nt in (("threads_1", 1), ("threads_all", os.cpu_count() or 1)):
+        best = None
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            Qc, Kc = O.compress(c, Q, K)
+            t1 = time.perf_counter()
+            sc = O.proxy_scores(c, Qc, Kc, nthreads=nt)
+            t2 = time.perf_counter()
+            mask = O.build_block_mask(sc, H, 1, P)
+            mask = mask[0] if isinstance(mask, tuple) else mask
+            t3 = time.perf_counter()
+            O.block_sparse_attention(Q, K, V, mask, S, nthreads=nt)
+            t4 = time.perf_counter()
+            st = {"compress_ms": (t1 - t0) * 1e3, "proxy_ms": (t2 - t1) * 1e3, "select_ms": (t3 - t2) * 1e3,
+                  "attention_ms": (t4 - t3) * 1e3, "total_ms": (t4 - t0) * 1e3}
+            if best is None or st["total_ms"] < best["total_ms"]:
+                best = st
+        best["threads"] = nt
+        out[label] = best
+    out["rho"] = float(1.0 - mask.sum() / (H * (L // S) * (L // S + 1) / 2))
+    return out
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -331,8 +377,10 @@ def main():
             if s >= args.warmup:
                 samples.append(ms)
         v = statistics.mean(samples)
+        c1 = cpu_c1_layer()
         out = dict(base, value=v, impl="reference", ms_per_step=v, config=config,
-                   cpu_baseline={"value": v, "unit": "ms/layer", "cores": cores, "kind": "port", "sample": sample},
+                   cpu_baseline={"value": v, "unit": "ms/layer", "cores": cores, "kind": "port", "sample": sample,
+                                 "c1_full_layer": c1},
                    e2e={"value": v, "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                    gpu_launches=0, detail=info)
         print(json.dumps(out), flush=True)
@@ -586,7 +634,8 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample, info = cpu_sample(args.config, gain, P)
-        cpu = {"value": v, "unit": "ms/layer", "cores": cores, "kind": "port", "sample": sample}
+        cpu = {"value": v, "unit": "ms/layer", "cores": cores, "kind": "port", "sample": sample,
+               "cpu_model": _cpu_model(), "c1_full_layer": cpu_c1_layer()}
     out = dict(base, value=ms, ms_per_step=ms, config=config, clocks=clk,
                e2e={"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": f"Engine.run_host(wait=False): pinned host Q/K/V -> H2D -> hot path -> D2H O, "
