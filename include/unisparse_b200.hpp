@@ -367,10 +367,11 @@ inline UniSparseResult unisparse_attn(const AttentionInputs& in, const Compressi
   return r;
 }
 
-inline AttentionOutput dense_attention(const AttentionInputs& in) {
+inline AttentionOutput dense_attention(const AttentionInputs& in, bool causal = true) {
   CompressionConfig c1;
   c1.c_q = c1.c_k = c1.c_h = 1;
-  const us_params p = detail::params(in, c1, true);
+  us_params p = detail::params(in, c1, true);
+  if (!causal) p.flags |= US_FLAG_NONCAUSAL;
   detail::validate("dense_attention", p, false);
   AttentionOutput out;
   out.O = DeviceBuffer<std::uint16_t>(size_t(in.B) * in.H * in.L * in.d_k);

@@ -11,7 +11,7 @@
  *   build_block_mask(scores,P,c_h,H) selection.hpp:41  us_build_block_mask
  *   block_sparse_attention(in, mask) attention.hpp:27  us_sparse_attention
  *   unisparse_attn(in, cfg)      pipeline.hpp:16       us_unisparse_attention
- *   dense_attention(in, causal)  attention.hpp:21      us_dense_attention (causal only)
+ *   dense_attention(in, causal)  attention.hpp:16      us_dense_attention (+ US_FLAG_NONCAUSAL)
  *   validate_inputs(in, cfg)     types.hpp:106         us_validate
  *   selection_flops(...)         metrics.hpp:31        us_selection_flops
  *   CompressionConfig / AttentionInputs types.hpp:54-72  us_params
@@ -71,7 +71,7 @@ enum { US_PROXY_UNISPARSE = 0, US_PROXY_ANTIDIAGONAL = 1, US_PROXY_LAST_BLOCK = 
 /* params.dtype */
 enum { US_DTYPE_BF16 = 0, US_DTYPE_F32 = 1 };
 /* params.flags */
-enum { US_FLAG_SYNC_CHECK = 1 };
+enum { US_FLAG_SYNC_CHECK = 1, US_FLAG_NONCAUSAL = 2 /* us_dense_attention: causal = false */ };
 
 /* CompressionConfig (types.hpp:54-62) + AttentionInputs dims (types.hpp:66-72)
  * + the GQA / batch / top-k extensions the north star adds. */
@@ -165,8 +165,9 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
                                  void* O, float* lse, const us_selection* sel, void* workspace,
                                  size_t workspace_bytes, void* stream);
 
-/* Causal dense attention through the same kernel with every causal block
- * selected (the P = 1 path; reference criterion 1). */
+/* dense_attention(in, causal) (attention.cpp:20-54): the same kernel with every
+ * causal block selected (the P = 1 path; reference criterion 1), or with every
+ * key block and no diagonal mask when params.flags has US_FLAG_NONCAUSAL. */
 us_status us_dense_attention(const us_params* p, const void* Q, const void* K, const void* V,
                              void* O, float* lse, void* workspace, size_t workspace_bytes,
                              void* stream);

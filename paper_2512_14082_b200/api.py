@@ -36,6 +36,7 @@ US_OK, US_ERR_INVALID_ARGUMENT, US_ERR_UNSUPPORTED, US_ERR_CUDA, US_ERR_INVALID_
 POOL_MEAN, POOL_MAX, POOL_STOCHASTIC = 0, 1, 2
 POST_SOFTMAX_BLOCK_CAUSAL, PRE_SOFTMAX_COMPRESSED_CAUSAL = 0, 1
 DTYPE_BF16, DTYPE_F32 = 0, 1
+FLAG_NONCAUSAL = 2
 SELECT_TOP_P, SELECT_TOP_K = 0, 1
 PROXY_UNISPARSE, PROXY_ANTIDIAGONAL, PROXY_LAST_BLOCK = 0, 1, 2
 FLAG_SYNC_CHECK = 1
@@ -382,7 +383,7 @@ def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: in
     O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
-    ws = workspace(p) if (validate_mask or Q.dtype == torch.float32) else None
+    ws = workspace(p) if (validate_mask or Q.dtype == torch.float32 or S != 64) else None
     _raise(lib().us_sparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(mask_bits.contiguous()),
                                      heads_per_plane, _ptr(O), _ptr(lse), _ptr(ws),
                                      ws.numel() if ws is not None else 0, _stream()))
@@ -407,10 +408,13 @@ def unisparse_attn(Q, K, V, cfg: CompressionConfig, S: int = 64, with_scores: bo
 
 
 @_on_input_device
-def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True):
-    """Causal dense attention via the same kernel with every causal block selected."""
+def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True, causal: bool = True):
+    """dense_attention(in, causal) (attention.cpp:20-54): the block-sparse kernel with
+    every causal block selected, or every key block (causal=False, no diagonal mask)."""
     _check_inputs(Q, K, V)
     p = make_params(Q, K, CompressionConfig(c_q=1, c_k=1, c_h=1), S)
+    if not causal:
+        p.flags |= FLAG_NONCAUSAL
     O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None

@@ -88,8 +88,9 @@ Checked check(const us_params& p, bool need_compression) {
   auto& u = c.unsupported;
   if (p.d_k != 64 && p.d_k != 128)
     u.push_back("d_k=" + std::to_string(p.d_k) + " unsupported on the GPU path (64 or 128)");
-  if (p.S != kGpuBlock) u.push_back("S=" + std::to_string(p.S) + " unsupported on the GPU path (64)");
-  if (p.L / std::max(p.S, 1) > 4096) u.push_back("N=L/S above 4096 unsupported on the GPU path");
+  if (p.S != kGpuBlock && p.S != 2 * kGpuBlock && p.S != 4 * kGpuBlock)
+    u.push_back("S=" + std::to_string(p.S) + " unsupported on the GPU path (64, 128 or 256)");
+  if (p.L / kGpuBlock > 4096) u.push_back("L/64 above 4096 unsupported on the GPU path");
   if ((long long)p.B * p.H * p.L >= (1ll << 31)) u.push_back("B*H*L must stay below 2^31 rows");
   if (need_compression) {
     if (p.strategy != US_POOL_MEAN && p.strategy != US_POOL_MAX && p.strategy != US_POOL_STOCHASTIC)
@@ -155,7 +156,7 @@ struct Geo {
 
 struct Ws {
   size_t err, first_bad, fb_count, absmax_q, absmax_k, exp_q, exp_k, fb_rows, qc, kc, qh, ql, kh,
-      kl, lse2, part, tmax, scores, mask, conv, total;
+      kl, lse2, part, tmax, scores, mask, conv, mask64, total;
   size_t header_bytes;  // [0, header_bytes) is cleared before each selection
 };
 
@@ -202,6 +203,9 @@ Ws layout(const us_params& p, bool scores_region = false) {
   w.mask = take(4 * rows * g.W);
   // f32 inputs: bf16 copies of Q, K, V for the attention kernels
   w.conv = p.dtype == US_DTYPE_F32 ? take(2 * (size_t(g.B) * g.H + 2 * size_t(g.B) * g.H_kv) * g.L * g.D) : 0;
+  // S > 64: the 64-granular copy of the block mask the attention kernels walk (one plane per head)
+  const size_t n64 = size_t(g.L) / kGpuBlock;
+  w.mask64 = g.S != kGpuBlock ? take(4 * size_t(g.B) * g.H * n64 * ((n64 + 31) / 32)) : 0;
   w.total = o;
   return w;
 }
@@ -435,33 +439,13 @@ int attention_pairing() {
   return v;
 }
 
-us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
-                        const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st,
-                        uint32_t* err = nullptr, int32_t* first_bad = nullptr, void* ws = nullptr) {
+// The attention kernels: bf16 Q/K/V, 64-granular masks (p.S == 64, p.dtype == bf16).
+us_status run_attention_core(const us_params& p, const void* Q, const void* K, const void* V,
+                             const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st, uint32_t* err,
+                             int32_t* first_bad) {
   Geo g(p);
-  if (p.dtype == US_DTYPE_F32) {
-    // the attention kernels compute on bf16 copies of f32 inputs (round to nearest even)
-    if (!ws) {
-      set_error("attention: f32 inputs need the workspace (us_workspace_bytes) for their bf16 copies");
-      return US_ERR_WORKSPACE;
-    }
-    Ws w = layout(p);
-    uint8_t* qb = at<uint8_t>(ws, w.conv);
-    uint8_t* kb = qb + size_t(2) * g.B * g.H * g.L * g.D;
-    uint8_t* vb = kb + size_t(2) * g.B * g.H_kv * g.L * g.D;
-    us_status s;
-    if ((s = launch_f32_to_bf16(static_cast<const float*>(Q), qb, (long long)g.B * g.H * g.L * g.D, st)) != US_OK)
-      return s;
-    if ((s = launch_f32_to_bf16(static_cast<const float*>(K), kb, (long long)g.B * g.H_kv * g.L * g.D, st)) != US_OK)
-      return s;
-    if ((s = launch_f32_to_bf16(static_cast<const float*>(V), vb, (long long)g.B * g.H_kv * g.L * g.D, st)) != US_OK)
-      return s;
-    us_params pb = p;
-    pb.dtype = US_DTYPE_BF16;
-    return run_attention(pb, qb, kb, vb, mask, hpp, O, lse, st, err, first_bad, nullptr);
-  }
-  CUtensorMap tQ, tK, tV;
   us_status s;
+  CUtensorMap tQ, tK, tV;
   if ((s = make_tmap_2d_16b(&tQ, Q, uint64_t(g.B) * g.H * g.L, g.D, 64, 64, true)) != US_OK) return s;
   if ((s = make_tmap_2d_16b(&tK, K, uint64_t(g.B) * g.H_kv * g.L, g.D, 64, 64, true)) != US_OK) return s;
   if ((s = make_tmap_2d_16b(&tV, V, uint64_t(g.B) * g.H_kv * g.L, g.D, 64, 64, true)) != US_OK) return s;
@@ -485,18 +469,62 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
   a.O = static_cast<__nv_bfloat16*>(O);
   a.lse = lse;
   a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  a.noncausal = (!mask && (p.flags & US_FLAG_NONCAUSAL)) ? 1 : 0;
   a.err = err;
   a.first_bad = first_bad;
   const int impl = attention_impl();
-  if (g.D == 128 && impl == 4) {
+  if (g.D == 128 && impl == 4 && !a.noncausal) {
     CUtensorMap tQ3;
     if ((s = make_tmap_rows_chunked(&tQ3, Q, uint64_t(g.B) * g.H * g.L, g.D, 64)) != US_OK) return s;
     return launch_attention_kt(a, tQ3, tK, tV3, st);
   }
-  if (impl == 2) return launch_attention2(a, tK, tV, st);
+  if (impl == 2 && !a.noncausal) return launch_attention2(a, tK, tV, st);
   a.one_tile = impl == 3 ? 1 : 0;
   return launch_attention(a, tQ, tK3, tV3, st);
 }
+
+us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
+                        const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st,
+                        uint32_t* err = nullptr, int32_t* first_bad = nullptr, void* ws = nullptr) {
+  Geo g(p);
+  us_params q = p;
+  if (p.S == kGpuBlock && p.dtype == US_DTYPE_BF16)
+    return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad);
+  if (!ws && (p.dtype == US_DTYPE_F32 || (mask && p.S != kGpuBlock))) {
+    set_error("attention: f32 inputs / S != 64 need the workspace (us_workspace_bytes)");
+    return US_ERR_WORKSPACE;
+  }
+  Ws w = layout(p);
+  us_status s;
+  if (p.S != kGpuBlock) {
+    // S = 64 m: the kernels walk 64-row / 64-key sub-blocks of the selected blocks
+    q.S = kGpuBlock;
+    if (mask) {
+      uint32_t* m64 = at<uint32_t>(ws, w.mask64);
+      if ((s = launch_mask_expand(mask, (long long)g.B * (g.H / hpp), g.N, g.W, g.S / kGpuBlock, m64, st)) != US_OK)
+        return s;
+      mask = m64;
+    }
+  }
+  if (p.dtype == US_DTYPE_F32) {
+    // the attention kernels compute on bf16 copies of f32 inputs (round to nearest even)
+    uint8_t* qb = at<uint8_t>(ws, w.conv);
+    uint8_t* kb = qb + size_t(2) * g.B * g.H * g.L * g.D;
+    uint8_t* vb = kb + size_t(2) * g.B * g.H_kv * g.L * g.D;
+    if ((s = launch_f32_to_bf16(static_cast<const float*>(Q), qb, (long long)g.B * g.H * g.L * g.D, st)) != US_OK)
+      return s;
+    if ((s = launch_f32_to_bf16(static_cast<const float*>(K), kb, (long long)g.B * g.H_kv * g.L * g.D, st)) != US_OK)
+      return s;
+    if ((s = launch_f32_to_bf16(static_cast<const float*>(V), vb, (long long)g.B * g.H_kv * g.L * g.D, st)) != US_OK)
+      return s;
+    q.dtype = US_DTYPE_BF16;
+    Q = qb;
+    K = kb;
+    V = vb;
+  }
+  return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad);
+}
+
 
 us_status sync_check(const us_params& p, void* ws, cudaStream_t st, const char* who) {
   Ws w = layout(p);
@@ -911,7 +939,8 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
       return s;
     if ((s = sync_check(*p, workspace, st, "block_sparse_attention")) != US_OK) return s;
   }
-  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK)
+  if ((p->dtype == US_DTYPE_F32 || p->S != kGpuBlock) &&
+      (s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK)
     return s;
   uint32_t* err = nullptr;
   int32_t* first_bad = nullptr;

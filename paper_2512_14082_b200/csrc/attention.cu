@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
   const int kvh = gr.h[0] / G;
   int jmax = -1;
   for (int k = 0; k < 4; ++k)
-    if (gr.en[k]) jmax = max(jmax, gr.i[k]);
+    if (gr.en[k]) jmax = max(jmax, a.noncausal ? a.N - 1 : gr.i[k]);
 
   if (threadIdx.x == 0) {
     for (int x = 0; x < 2; ++x) {
@@ -263,11 +263,13 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       const uint32_t* src =
           a.mask ? a.mask + ((long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + ig) * a.W
                  : nullptr;
+      // (non-causal dense attention, dense_attention(in, false): every key block j < N)
+      const int jlast = a.noncausal ? a.N - 1 : ig;
       for (int w = lane; w < nw; w += 32) {
         uint32_t word = 0;
-        if (gr.en[g] && (w << 5) <= ig) {
+        if (gr.en[g] && (w << 5) <= jlast) {
           word = src ? src[w] : ~0u;
-          const int hi = ig - (w << 5);  // bits 0..hi are causal
+          const int hi = jlast - (w << 5);  // bits 0..hi are attended
           if (hi < 31) word &= (2u << hi) - 1u;
         }
         mrow[g][w] = word;
@@ -535,7 +537,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       bool pv_prev_done = (k == 0);
       uint32_t packed[kBS / 2];
       if (sel) {
-        const bool diag = (j == ig);
+        const bool diag = (j == ig) && !a.noncausal;
         if (diag) {
 #pragma unroll
           for (int c = 0; c < kBS; ++c)

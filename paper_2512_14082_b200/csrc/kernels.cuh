@@ -144,6 +144,7 @@ struct AttnArgs {
   int one_tile;         // 1: one M=128 tile (two groups) per CTA, two CTAs per SM
   uint32_t* err;        // device error word (nullable): |= 4 non-causal bit, |= 8 empty row
   int32_t* first_bad;   // first offending mask row (atomicMin; nullable with err)
+  int noncausal;        // 1: dense_attention(in, causal = false): all N key blocks, no diagonal mask
 };
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);
@@ -171,6 +172,11 @@ us_status launch_block_recall(int B, int H, int N, int W, int planes, int heads_
                               cudaStream_t st);
 us_status launch_row_spearman(int B, int H, int N, int c_h, const float* proxy, const float* ref, double* rows_ws,
                               uint8_t* defined, double* out, long long* n_def, cudaStream_t st);
+
+// S = 64 m block masks [planes][N][W] -> 64-granular masks [planes][N m][ceil(N m / 32)]
+// (sub-blocks of the diagonal block wholly in the future dropped), for the attention kernels.
+us_status launch_mask_expand(const uint32_t* in, long long planes, int N, int W, int m, uint32_t* out,
+                             cudaStream_t st);
 
 // mask validation: err |= 4 for a non-causal bit, 8 for an empty causal row;
 // first offending row index (b*planes+p)*N+i recorded with atomicMin in *first_bad.

@@ -162,6 +162,10 @@ us_status launch_lb_t(const LastBlockArgs& a, cudaStream_t st) {
 }  // namespace
 
 us_status launch_last_block_probe(const LastBlockArgs& a, cudaStream_t st) {
+  if (a.N * kRowsLB != a.L) {
+    set_error("select_blocks: the last-block probe runs at block size S = 64 on the GPU path");
+    return US_ERR_UNSUPPORTED;
+  }
   if (a.L % kChunk != 0) {
     set_error("select_blocks: the last-block probe needs L divisible by 256 on the GPU path");
     return US_ERR_UNSUPPORTED;

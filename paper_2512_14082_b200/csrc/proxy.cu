@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(320, 1)
 // (select.cu, launch_select_fused).
 template <int SW, int RQ, int SPB>
 __global__ void __launch_bounds__(256) proxy_finalize_kernel(const ProxyArgs a) {
-  __shared__ float lse_sh[64];
+  __shared__ float lse_sh[128];
   const int i = gridDim.x - 1 - blockIdx.x;
   const int plane = blockIdx.y;
   const int rq = RQ > 0 ? RQ : a.rq;
@@ -356,8 +356,8 @@ us_status launch_proxy_d(const ProxyArgs& a, const CUtensorMap& tmKh, const CUte
 int proxy_slot_width(int rk) { return rk >= 8 ? 8 : rk; }
 
 us_status launch_proxy(const ProxyArgs& a, const CUtensorMap& tmKh, const CUtensorMap& tmKl, cudaStream_t st) {
-  if (a.rq > 64) {
-    set_error("proxy: S/c_q above 64 unsupported");
+  if (a.rq > 128) {
+    set_error("proxy: S/c_q above 128 unsupported");
     return US_ERR_UNSUPPORTED;
   }
   if (a.D == 128) return launch_proxy_d<128>(a, tmKh, tmKl, st);

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
   extern __shared__ __align__(16) uint8_t fsm[];
   float* sc = reinterpret_cast<float*>(fsm);
   uint32_t* hist = reinterpret_cast<uint32_t*>(fsm + size_t(sa.N) * 4);
-  __shared__ float lse_sh[64];
+  __shared__ float lse_sh[128];
   __shared__ double dsh[kFusedWarps];
   __shared__ int ish[kFusedWarps];
   __shared__ int wcnt[kFusedMaxW], wpre[kFusedMaxW];
@@ -624,7 +624,7 @@ template <int SW, int RQ, int SPB>
 __global__ void __launch_bounds__(256) select_fallback_fused_kernel(const ProxyArgs pa, SelectArgs a) {
   __shared__ unsigned long long keys[kFbMaxN];
   __shared__ uint8_t flag[kFbMaxN];
-  __shared__ float lse_sh[64];
+  __shared__ float lse_sh[128];
   __shared__ int sh_k;
   __shared__ double sh_cov;
   const int count = *a.fb_count;
@@ -749,6 +749,34 @@ __global__ void mask_check_kernel(const uint32_t* mask, int rows, int N, int W, 
   }
 }
 
+// S = 64 m block masks -> the 64-granular masks the attention kernels walk: query
+// sub-block ii = i m + a keeps key sub-block jj = j m + b iff block (i, j) is selected,
+// except the sub-blocks of the diagonal block that lie wholly in the future (j == i,
+// b > a) — token-level causality inside the diagonal block is then exactly the
+// 64-granular kernel's (attention.cpp:117-118). Non-causal source bits (j > i) are
+// kept, so the kernels' mask checks still see them.
+__global__ void mask_expand_kernel(const uint32_t* __restrict__ in, long long rows64, int N, int W, int m,
+                                   int N64, int W64, uint32_t* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows64 * W64) return;
+  const int w64 = int(t % W64);
+  const long long r64 = t / W64;
+  const int ii = int(r64 % N64);
+  const long long plane = r64 / N64;
+  const int i = ii / m;
+  const uint32_t* src = in + (plane * N + i) * W;
+  uint32_t word = 0;
+#pragma unroll 4
+  for (int b = 0; b < 32; ++b) {
+    const int jj = w64 * 32 + b;
+    if (jj >= N64) break;
+    const int j = jj / m;
+    const bool sel = (src[j >> 5] >> (j & 31)) & 1u;
+    if (sel && !(j == i && jj > ii)) word |= 1u << b;
+  }
+  out[t] = word;
+}
+
 template <int NPL>
 void launch_sel(const SelectArgs& a, cudaStream_t st) {
   const int threads = 256, wpc = threads / 32;
@@ -793,6 +821,15 @@ us_status launch_select_fused(const ProxyArgs& pa, const SelectArgs& sa, cudaStr
   else launch_fused_t<1, 0, 0>(pa, sa, st);
   US_LAUNCH_CHECK("select_fused_kernel");
   if (sa.select_mode == US_SELECT_TOP_P) US_LAUNCH_CHECK("select_fallback_fused_kernel");
+  return US_OK;
+}
+
+us_status launch_mask_expand(const uint32_t* in, long long planes, int N, int W, int m, uint32_t* out,
+                             cudaStream_t st) {
+  const int N64 = N * m, W64 = (N64 + 31) / 32;
+  const long long n = planes * N64 * W64;
+  mask_expand_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(in, planes * N64, N, W, m, N64, W64, out);
+  US_LAUNCH_CHECK("mask_expand_kernel");
   return US_OK;
 }
 

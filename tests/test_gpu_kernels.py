@@ -241,6 +241,24 @@ def test_dense_attention_matches_oracle_and_sdpa():
     assert np.abs(Og - ref).max() <= ATOL
 
 
+@pytest.mark.parametrize("H,H_kv,d", [(4, 2, 128), (2, 2, 64)])
+def test_dense_attention_noncausal_matches_oracle(H, H_kv, d):
+    """dense_attention(in, causal = false) (attention.cpp:20-54): every key block,
+    no diagonal mask; vs the fp64 oracle and torch fp32 SDPA without a causal mask."""
+    rng = np.random.default_rng(9 + d)
+    B, L = 1, 1024
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    Og, lseg = us().dense_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), causal=False)
+    Or, lser = O.dense_attention(Q[0], K[0], V[0], causal=False)
+    assert np.abs(Og.float().cpu().numpy()[0] - Or).max() <= ATOL
+    assert np.abs(lseg.cpu().numpy()[0] - lser).max() <= 1e-3
+    q = torch.from_numpy(Q).cuda()
+    k = torch.from_numpy(K).cuda().repeat_interleave(H // H_kv, 1)
+    v = torch.from_numpy(V).cuda().repeat_interleave(H // H_kv, 1)
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=False).cpu().numpy()
+    assert np.abs(Og.float().cpu().numpy() - ref).max() <= ATOL
+
+
 def test_sparse_attention_large_logits_finite():
     rng = np.random.default_rng(3)
     Q, K, V = _rand_qkv(rng, 1, 2, 1, 512, 128, scale=30.0)

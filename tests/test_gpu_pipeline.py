@@ -283,3 +283,32 @@ def test_fuzz_pipeline_against_oracle(case):
     Og = res.O.float().cpu().numpy()[0]
     Or, _ = O.block_sparse_attention(Q, K, V, g_mask, 64)
     assert np.abs(Og - Or).max() <= 1e-2 * np.abs(Or).max() + 1e-4
+
+
+@pytest.mark.parametrize("S,d,mode,c", [(128, 64, 0, 8), (128, 128, 0, 8), (128, 64, 1, 8), (128, 128, 0, 16),
+                                        (256, 64, 0, 16)])
+def test_block_size_above_64_matches_oracle(S, d, mode, c):
+    """S = 128 (the reference acceptance battery's block size, acceptance.cpp:53-60) and
+    S = 256: compress / proxy / select run at block size S (rq = S / c_q composite rows
+    per block); attention walks the 64-granular expansion of the S-block mask, whose
+    diagonal S-block keeps exactly the token-level causal pairs (attention.cpp:117-118).
+    Masks bit-exact and outputs within the bf16 tolerance vs the oracle at the same S."""
+    L, H, H_kv = 4096, 4, 2
+    Q, K, V, _ = O.gen_workload(O.WL_PLANTED, L, H, d, S, 77 + S + d, H_kv=H_kv, gain=8.0)
+    Q, K, V = O.bf16_round(Q), O.bf16_round(K), O.bf16_round(V)
+    cfg = us().CompressionConfig(P=0.95, causal_mode=mode, c_q=c, c_k=c)
+    res = us().unisparse_attn(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1), cfg, S=S)
+    torch.cuda.synchronize()
+    gmask = res.report.mask.dense_mask()[0].cpu().numpy()
+    c_o = O.cfg(H, L, d, S, H_kv=H_kv, P=0.95, causal_mode=mode, c_q=c, c_k=c)
+    Or, lser, ref_mask, _ = O.unisparse_attn(c_o, Q, K, V)
+    assert gmask.shape == ref_mask.shape == (H, L // S, L // S)
+    assert int((gmask != ref_mask).sum()) == 0
+    Og = res.O[0].float().cpu().numpy()
+    assert np.abs(Og - Or).max() <= 1e-2 * np.abs(Or).max() + 1e-4
+    assert np.linalg.norm(Og - Or) / np.linalg.norm(Or) <= 1e-2
+    assert np.abs(res.lse[0].cpu().numpy() - lser).max() <= 2e-3 * max(1.0, np.abs(lser).max())
+    # block_sparse_attention on the S-block mask directly equals the pipeline's attention
+    O2, _ = us().block_sparse_attention(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1),
+                                        res.report.mask.mask_bits, heads_per_plane=1, S=S)
+    assert torch.equal(O2, res.O)
