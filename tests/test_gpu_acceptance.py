@@ -2,8 +2,9 @@
 on the GPU path. Inputs come from the bit-faithful port of the reference
 generator (oracle, CPU) rounded to bf16; every score, mask, output and metric is
 computed on the device. Deviations from the reference battery, all forced by the
-GPU path's envelope: block size S = 64 (the reference uses 128), d_k in
-{64, 128} (the reference also runs 32), and criterion 2's score tolerance is
+GPU path's envelope: d_k in {64, 128} (the reference also runs 32); block size
+S = 128 as the reference battery, except criterion 6 at S = 64 (the GPU
+last-block probe's block size), and criterion 2's score tolerance is
 fp32-class (two different fp32 computations of the same fp64 quantity) instead
 of 1e-6. Each criterion prints its PASS/FAIL line like acceptance.cpp and the
 measured values land in gpurun_out/acceptance_gpu.json."""
@@ -19,7 +20,8 @@ from gpu_util import to_dev_bf16
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-S = 64
+S = 128  # the reference battery's block size (acceptance.cpp:53-60)
+S6 = 64  # criterion 6: the last-block probe runs at S = 64 on the GPU path
 RESULTS = {}
 
 
@@ -36,7 +38,7 @@ def _report(n, name, ok, detail):
         json.dump(RESULTS, f, indent=1)
 
 
-def _inputs(kind, L, H, d, seed, **kw):
+def _inputs(kind, L, H, d, seed, S=S, **kw):
     Q, K, V, planted = O.gen_workload(kind, L, H, d, S, seed, **kw)
     return to_dev_bf16(O.bf16_round(Q), 1), to_dev_bf16(O.bf16_round(K), 1), to_dev_bf16(O.bf16_round(V), 1), planted
 
@@ -59,8 +61,8 @@ def test_criterion_1_degenerate_top_p_equals_dense():
         Q, K, V, _ = O.gen_workload(O.WL_GAUSSIAN, L, H, d, S, seed, H_kv=H_kv)
         Q, K, V = O.bf16_round(Q), O.bf16_round(K), O.bf16_round(V)
         q, k, v = to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1)
-        r = us().unisparse_attn(q, k, v, us().CompressionConfig(P=1.0))
-        dense, _ = us().dense_attention(q, k, v)
+        r = us().unisparse_attn(q, k, v, us().CompressionConfig(P=1.0), S=S)
+        dense, _ = us().dense_attention(q, k, v, S=S)
         Od, _ = O.dense_attention(Q, K, V)
         N = L // S
         e_sp = np.abs(r.O.float().cpu().numpy()[0] - Od)
@@ -83,15 +85,15 @@ def test_criterion_2_identity_compression_reproduces_exact_mass():
         L, H, d = (256, 512, 1024)[i % 3], (1, 2)[(i // 3) % 2], (64, 128)[(i // 6) % 2]
         q, k, _, _ = _inputs(O.WL_GAUSSIAN, L, H, d, 2000 + i)
         cfg = us().CompressionConfig(c_q=1, c_k=1, c_h=1, causal_mode=us().PRE_SOFTMAX_COMPRESSED_CAUSAL)
-        sc = us().select_blocks(q, k, cfg, with_scores=True).mask.scores[0]
-        mass = us().exact_block_mass(q, k)[0]
+        sc = us().select_blocks(q, k, cfg, S=S, with_scores=True).mask.scores[0]
+        mass = us().exact_block_mass(q, k, S=S)[0]
         N = L // S
         tri = torch.tril(torch.ones(N, N, dtype=torch.bool, device=sc.device))
         worst = max(worst, (sc - mass).abs()[:, tri].max().item())
         for P in (0.5, 0.7, 0.9, 0.95):
             c = us().CompressionConfig(c_q=1, c_k=1, c_h=1, P=P)
-            a = us().build_block_mask(sc.unsqueeze(0).contiguous(), c).dense_mask(H)
-            b = us().build_block_mask(mass.masked_fill(~tri, 0.0).unsqueeze(0).contiguous(), c).dense_mask(H)
+            a = us().build_block_mask(sc.unsqueeze(0).contiguous(), c, S=S).dense_mask(H)
+            b = us().build_block_mask(mass.masked_fill(~tri, 0.0).unsqueeze(0).contiguous(), c, S=S).dense_mask(H)
             n = int((a != b).sum().item())
             flips += n
             masks_ok &= n == 0
@@ -106,11 +108,11 @@ def test_criterion_3_compressed_rankings_track_oracle():
     for L in (2048, 4096):
         for seed in (31, 32, 33):
             q, k, _, _ = _inputs(O.WL_PLANTED, L, 2, 64, seed)
-            mass = us().exact_block_mass(q, k)
+            mass = us().exact_block_mass(q, k, S=S)
             for ci, c in enumerate(cs):
                 cfg = us().CompressionConfig(c_q=c, c_k=c, seed=seed, causal_mode=us().PRE_SOFTMAX_COMPRESSED_CAUSAL)
-                sc = us().select_blocks(q, k, cfg, with_scores=True).mask.scores
-                rho = us().mean_row_spearman(sc, mass, 1)[0]
+                sc = us().select_blocks(q, k, cfg, S=S, with_scores=True).mask.scores
+                rho = us().mean_row_spearman(sc, mass, 1, S=S)[0]
                 grand[ci] += rho
                 if c == 8:
                     min_c8 = min(min_c8, rho)
@@ -127,7 +129,7 @@ def test_criterion_4_sparsity_monotone_in_p_with_coverage():
     q, k, _, _ = _inputs(O.WL_PLANTED, 1024, 2, 64, 41)
     prev, mono, cov, zero, rhos = 1.0, True, True, True, []
     for P in (0.7, 0.8, 0.9, 0.95, 1.0):
-        rep = us().select_blocks(q, k, us().CompressionConfig(P=P, seed=41))
+        rep = us().select_blocks(q, k, us().CompressionConfig(P=P, seed=41), S=S)
         mono &= rep.rho_mean <= prev
         cov &= rep.mask.coverage.min().item() >= P - 1e-12
         if P == 1.0:
@@ -143,11 +145,11 @@ def test_criterion_5_output_fidelity_at_operating_points():
     w95, w90, wrec = 1.0, 1.0, 1.0
     for seed in (51, 52, 53):
         q, k, v, planted = _inputs(O.WL_PLANTED, 2048, 2, 64, seed)
-        dense, _ = us().dense_attention(q, k, v)
-        r95 = us().unisparse_attn(q, k, v, us().CompressionConfig(P=0.95, seed=seed))
+        dense, _ = us().dense_attention(q, k, v, S=S)
+        r95 = us().unisparse_attn(q, k, v, us().CompressionConfig(P=0.95, seed=seed), S=S)
         w95 = min(w95, us().output_fidelity(r95.O, dense)["cosine"])
-        wrec = min(wrec, us().planted_recall(r95.report.mask.mask_bits, torch.from_numpy(planted).cuda()))
-        r90 = us().unisparse_attn(q, k, v, us().CompressionConfig(P=0.9, seed=seed))
+        wrec = min(wrec, us().planted_recall(r95.report.mask.mask_bits, torch.from_numpy(planted).cuda(), S=S))
+        r90 = us().unisparse_attn(q, k, v, us().CompressionConfig(P=0.9, seed=seed), S=S)
         w90 = min(w90, us().output_fidelity(r90.O, dense)["cosine"])
     ok = w95 >= 0.99 and w90 >= 0.98 and wrec >= 0.95
     _report(5, "output-fidelity-operating-points", ok,
@@ -158,11 +160,11 @@ def test_criterion_5_output_fidelity_at_operating_points():
 def test_criterion_6_unisparse_beats_last_block_probe_at_matched_sparsity():
     wins = matched = 0
     H, L = 2, 2048
-    N = L // S
+    N = L // S6
     for s in range(20):
-        q, k, _, _ = _inputs(O.WL_LOCALITY_SHIFT, L, H, 64, 60 + s)
-        mass = us().exact_block_mass(q, k)
-        uni = us().select_blocks(q, k, us().CompressionConfig(P=0.95, seed=60 + s))
+        q, k, _, _ = _inputs(O.WL_LOCALITY_SHIFT, L, H, 64, 60 + s, S=S6)
+        mass = us().exact_block_mass(q, k, S=S6)
+        uni = us().select_blocks(q, k, us().CompressionConfig(P=0.95, seed=60 + s), S=S6)
         rho_u = uni.rho_mean
         probe = us().select_blocks(q, k, us().CompressionConfig(P=0.95), with_scores=True,
                                    proxy=us().api.PROXY_LAST_BLOCK).mask.scores
@@ -192,13 +194,13 @@ def test_criterion_8_mean_pooling_wins_the_strategy_ablation():
     wins = 0
     for s in range(20):
         q, k, _, _ = _inputs(O.WL_PLANTED, 1024, 2, 64, 80 + s)
-        mass = us().exact_block_mass(q, k)
+        mass = us().exact_block_mass(q, k, S=S)
         rho = []
         for strat in (0, 1, 2):
             cfg = us().CompressionConfig(strategy=strat, P=0.95, seed=80 + s,
                                          causal_mode=us().PRE_SOFTMAX_COMPRESSED_CAUSAL)
-            sc = us().select_blocks(q, k, cfg, with_scores=True).mask.scores
-            rho.append(us().mean_row_spearman(sc, mass, 1)[0])
+            sc = us().select_blocks(q, k, cfg, S=S, with_scores=True).mask.scores
+            rho.append(us().mean_row_spearman(sc, mass, 1, S=S)[0])
         wins += rho[0] >= rho[1] and rho[0] >= rho[2]
     ok = wins >= 16
     _report(8, "pooling-strategy-ablation-direction", ok, f"{wins}/20 wins")
