@@ -18,6 +18,7 @@ without the CUDA library every call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import dataclasses
 import functools
@@ -89,52 +90,96 @@ _lib = None
 _lib_lock = threading.Lock()
 
 
+def _bind(L: C.CDLL) -> C.CDLL:
+    L.us_version.restype = C.c_char_p
+    L.us_last_error.restype = C.c_char_p
+    L.us_validate.argtypes = [C.POINTER(UsParams), C.c_char_p, C.c_size_t]
+    L.us_workspace_bytes.restype = C.c_size_t
+    L.us_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+    vp = C.c_void_p
+    L.us_compress.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.c_size_t, vp]
+    L.us_select.argtypes = [C.POINTER(UsParams), vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
+    L.us_build_block_mask.argtypes = [C.POINTER(UsParams), vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
+    L.us_select_proxy.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp, vp, C.POINTER(UsSelection),
+                                  vp, C.c_size_t, vp]
+    L.us_proxy_workspace_bytes.restype = C.c_size_t
+    L.us_proxy_workspace_bytes.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32]
+    L.us_sparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_size_t, vp]
+    L.us_unisparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.POINTER(UsSelection), vp,
+                                         C.c_size_t, vp]
+    L.us_dense_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+    L.us_check_device_errors.argtypes = [C.POINTER(UsParams), vp, vp]
+    L.us_selection_flops.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp]
+    L.us_last_launch_count.restype = C.c_int32
+    L.us_write_tensor.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32]
+    L.us_read_tensor_header.argtypes = [C.c_char_p, vp, vp, vp]
+    L.us_read_tensor.argtypes = [C.c_char_p, vp, C.c_size_t]
+    L.us_save_mask_json.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32, C.c_double]
+    L.us_load_mask_json.argtypes = [C.c_char_p, vp, vp, vp, vp, C.c_size_t]
+    L.us_profile_enable.argtypes = [C.c_int32]
+    L.us_profile_read.argtypes = [C.c_void_p, C.c_int32]
+    L.us_profile_read.restype = C.c_int32
+    L.us_mass_workspace_bytes.restype = C.c_size_t
+    L.us_mass_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+    L.us_metrics_workspace_bytes.restype = C.c_size_t
+    L.us_metrics_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+    L.us_exact_block_mass.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
+    L.us_output_fidelity.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
+    L.us_block_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
+    L.us_mean_row_spearman.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+    L.us_planted_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
+    L.us_set_attention_impl.argtypes = [C.c_int32]
+    if hasattr(L, "us_selftest_umma"):
+        L.us_selftest_umma.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]
+    return L
+
+
+_product = None
+
+
 def lib() -> C.CDLL:
-    global _lib
+    """The library every operator of this module calls: the product build, or the
+    calibration build inside a `calibration()` block."""
+    global _lib, _product
     with _lib_lock:
         if _lib is None:
             if not os.path.exists(LIB_PATH):
                 raise CudaError(f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
-            _lib = C.CDLL(LIB_PATH)
-            L = _lib
-            L.us_version.restype = C.c_char_p
-            L.us_last_error.restype = C.c_char_p
-            L.us_validate.argtypes = [C.POINTER(UsParams), C.c_char_p, C.c_size_t]
-            L.us_workspace_bytes.restype = C.c_size_t
-            L.us_workspace_bytes.argtypes = [C.POINTER(UsParams)]
-            vp = C.c_void_p
-            L.us_compress.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.c_size_t, vp]
-            L.us_select.argtypes = [C.POINTER(UsParams), vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
-            L.us_build_block_mask.argtypes = [C.POINTER(UsParams), vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
-            L.us_select_proxy.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp, vp, C.POINTER(UsSelection),
-                                          vp, C.c_size_t, vp]
-            L.us_proxy_workspace_bytes.restype = C.c_size_t
-            L.us_proxy_workspace_bytes.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32]
-            L.us_sparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_size_t, vp]
-            L.us_unisparse_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
-            L.us_dense_attention.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
-            L.us_check_device_errors.argtypes = [C.POINTER(UsParams), vp, vp]
-            L.us_selection_flops.argtypes = [C.POINTER(UsParams), C.c_int32, C.c_int32, vp]
-            L.us_selftest_umma.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]
-            L.us_last_launch_count.restype = C.c_int32
-            L.us_write_tensor.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32]
-            L.us_read_tensor_header.argtypes = [C.c_char_p, vp, vp, vp]
-            L.us_read_tensor.argtypes = [C.c_char_p, vp, C.c_size_t]
-            L.us_save_mask_json.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32, C.c_double]
-            L.us_load_mask_json.argtypes = [C.c_char_p, vp, vp, vp, vp, C.c_size_t]
-            L.us_profile_enable.argtypes = [C.c_int32]
-            L.us_profile_read.argtypes = [C.c_void_p, C.c_int32]
-            L.us_profile_read.restype = C.c_int32
-            L.us_mass_workspace_bytes.restype = C.c_size_t
-            L.us_mass_workspace_bytes.argtypes = [C.POINTER(UsParams)]
-            L.us_metrics_workspace_bytes.restype = C.c_size_t
-            L.us_metrics_workspace_bytes.argtypes = [C.POINTER(UsParams)]
-            L.us_exact_block_mass.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
-            L.us_output_fidelity.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, C.c_size_t, vp]
-            L.us_block_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
-            L.us_mean_row_spearman.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
-            L.us_planted_recall.argtypes = [C.POINTER(UsParams), vp, C.c_int32, vp, C.c_int32, vp, vp, C.c_size_t, vp]
+            _lib = _product = _bind(C.CDLL(LIB_PATH))
         return _lib
+
+
+CALIB_LIB_PATH = os.path.join(_PKG, "_build", "libunisparse_b200_calib.so")
+_calib = None
+
+
+def calib_lib() -> C.CDLL:
+    """The calibration build (-DUS_CALIBRATION): the product plus the measured-slower
+    attention variants (us_set_attention_impl 2-4) and the hardware probes
+    (us_selftest_*). Loaded separately (RTLD_LOCAL), never the default path."""
+    global _calib
+    with _lib_lock:
+        if _calib is None:
+            if not os.path.exists(CALIB_LIB_PATH):
+                raise CudaError(f"calibration library not built: {CALIB_LIB_PATH}")
+            _calib = _bind(C.CDLL(CALIB_LIB_PATH))
+        return _calib
+
+
+@contextlib.contextmanager
+def calibration():
+    """Route this module's operators through the calibration library for the block."""
+    global _lib
+    lib()
+    cal = calib_lib()
+    with _lib_lock:
+        prev = _lib
+        _lib = cal
+    try:
+        yield cal
+    finally:
+        with _lib_lock:
+            _lib = prev
 
 
 def _raise(status: int, default: str = ""):
@@ -564,8 +609,12 @@ class Engine:
 
 
 def selftest_umma(mode: int, N: int, bf16: bool, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """Single-tile tcgen05 operand-path check (calibration build, csrc/selftest.cu)."""
     D = torch.empty((128, N), dtype=torch.float32, device=A.device)
-    _raise(lib().us_selftest_umma(mode, N, int(bf16), _ptr(A), _ptr(B), _ptr(D), _stream()))
+    L = calib_lib()
+    rc = L.us_selftest_umma(mode, N, int(bf16), _ptr(A), _ptr(B), _ptr(D), _stream())
+    if rc:
+        raise CudaError(f"status {rc}: {L.us_last_error().decode()}")
     return D
 
 

@@ -1,4 +1,9 @@
-"""Builds the sm_100a shared library in-tree: paper_2512_14082_b200/_build/libunisparse_b200.so.
+"""Builds the sm_100a shared libraries in-tree:
+  paper_2512_14082_b200/_build/libunisparse_b200.so        the product (the hot path + the C ABI)
+  paper_2512_14082_b200/_build/libunisparse_b200_calib.so  calibration build (-DUS_CALIBRATION):
+      the product plus the measured-slower attention variants (attention2.cu, the one-tile
+      attention.cu instantiation, the key-major attention_kt.cu) and the tcgen05 / TMEM /
+      MUFU probes (selftest.cu) — for tests/tools that select them, never the default path.
 
 nvcc cross-compiles without a GPU; the .so travels to the GPU box with the
 repo snapshot (git-ignored, not gpurun-ignored).
@@ -15,7 +20,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "libunisparse_b200.so")
-SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "attention_kt.cu", "attention2.cu", "lastblock.cu", "io.cu", "metrics.cu", "selftest.cu"]
+SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "lastblock.cu", "io.cu", "metrics.cu"]
+CALIB_SOURCES = SOURCES + ["attention2.cu", "attention_kt.cu", "selftest.cu"]
+CALIB_LIB = os.path.join(OUT_DIR, "libunisparse_b200_calib.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -29,18 +36,15 @@ def _newer(target: str, deps) -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OUT_DIR, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))]
-    headers.append(os.path.join(os.path.dirname(PKG), "include", "us_api.h"))
-    objs = []
-    jobs = []
-    for src in SOURCES:
+def _build_lib(sources, obj_dir, lib, defines, headers, force, verbose):
+    os.makedirs(obj_dir, exist_ok=True)
+    objs, jobs = [], []
+    for src in sources:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+        o = os.path.join(obj_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or not _newer(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *FLAGS, *defines, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -52,8 +56,17 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or not _newer(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda" if False else "-lrt"])
+    if force or jobs or not _newer(lib, objs):
+        run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lrt"])
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    os.makedirs(OUT_DIR, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))]
+    headers.append(os.path.join(os.path.dirname(PKG), "include", "us_api.h"))
+    _build_lib(SOURCES, OUT_DIR, LIB, [], headers, force, verbose)
+    _build_lib(CALIB_SOURCES, os.path.join(OUT_DIR, "calib"), CALIB_LIB, ["-DUS_CALIBRATION"], headers, force,
+               verbose)
     build_wrapper_test(force)
     return LIB
 

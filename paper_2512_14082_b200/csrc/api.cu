@@ -473,6 +473,8 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   a.err = err;
   a.first_bad = first_bad;
   const int impl = attention_impl();
+#ifdef US_CALIBRATION
+  // calibration variants (libunisparse_b200_calib.so only; measured slower, DESIGN.md §3 a6)
   if (g.D == 128 && impl == 4 && !a.noncausal) {
     CUtensorMap tQ3;
     if ((s = make_tmap_rows_chunked(&tQ3, Q, uint64_t(g.B) * g.H * g.L, g.D, 64)) != US_OK) return s;
@@ -480,6 +482,9 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   }
   if (impl == 2 && !a.noncausal) return launch_attention2(a, tK, tV, st);
   a.one_tile = impl == 3 ? 1 : 0;
+#else
+  (void)impl;
+#endif
   return launch_attention(a, tQ, tK3, tV3, st);
 }
 
@@ -602,6 +607,13 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
 }
 
 us_status us_set_attention_impl(int32_t impl) {
+#ifndef US_CALIBRATION
+  if (impl >= 2) {
+    set_error("us_set_attention_impl: implementations 2-4 are calibration variants, present only in "
+              "libunisparse_b200_calib.so");
+    return US_ERR_UNSUPPORTED;
+  }
+#endif
   if (impl < 0 || impl > 4) {
     set_error("us_set_attention_impl: impl must be 0 (automatic), 1 (two query tiles per CTA), 2 (128-key steps), "
               "3 (one tile per CTA) or 4 (key-major)");

@@ -697,10 +697,13 @@ us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUte
     set_error("attention: N (=L/S) above 4096 is not supported on the GPU path");
     return US_ERR_UNSUPPORTED;
   }
+#ifdef US_CALIBRATION
   if (a.one_tile) {
     if (a.D == 128) return launch_attn_t<128, 1>(a, tmQ, tmK, tmV, st);
     if (a.D == 64) return launch_attn_t<64, 1>(a, tmQ, tmK, tmV, st);
-  } else {
+  } else
+#endif
+  {
     if (a.D == 128) return launch_attn_t<128, 2>(a, tmQ, tmK, tmV, st);
     if (a.D == 64) return launch_attn_t<64, 2>(a, tmQ, tmK, tmV, st);
   }

@@ -298,9 +298,8 @@ def test_attention_impls_agree(H, H_kv, d):
     mask &= np.tril(np.ones((N, N), bool))
     mask[..., np.arange(N), np.arange(N)] = True
     bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
-    lib = us().api.lib()
-    lib.us_set_attention_impl.argtypes = [ctypes.c_int32]
-    try:
+    with us().api.calibration() as lib:  # the variants live in the calibration build
+      try:
         for impl in ((4, 3, 2, 1) if d == 128 else (3, 2, 1)):
             assert lib.us_set_attention_impl(impl) == 0
             Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
@@ -311,15 +310,22 @@ def test_attention_impls_agree(H, H_kv, d):
                 assert np.abs(Og[b] - Or).max() <= ATOL, (impl, b)
                 assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO, (impl, b)
                 assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
-    finally:
+      finally:
         lib.us_set_attention_impl(0)
 
 
-def _set_impl(impl):
-    import ctypes
+def test_product_library_has_no_calibration_variants():
+    """The product library runs attention.cu only: the calibration variants (2-4) and the
+    probes are absent from libunisparse_b200.so (they live in the calibration build)."""
     lib = us().api.lib()
-    lib.us_set_attention_impl.argtypes = [ctypes.c_int32]
-    assert lib.us_set_attention_impl(impl) == 0
+    assert lib.us_set_attention_impl(2) == us().api.US_ERR_UNSUPPORTED
+    assert lib.us_set_attention_impl(4) == us().api.US_ERR_UNSUPPORTED
+    assert lib.us_set_attention_impl(0) == 0
+    assert not hasattr(lib, "us_selftest_umma")
+
+
+def _set_impl(impl):
+    assert us().api.lib().us_set_attention_impl(impl) == 0
 
 
 @pytest.mark.parametrize("growth", [0.0, 1.0, -1.0])
@@ -343,11 +349,12 @@ def test_attention_kt_offset_moves(growth):
     mask[empty, 0] = True
     bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
     for impl in (4, 1):
-        _set_impl(impl)
-        try:
-            Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
-        finally:
-            _set_impl(0)
+        with us().api.calibration():
+            _set_impl(impl)
+            try:
+                Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
+            finally:
+                _set_impl(0)
         Og = Og.float().cpu().numpy()
         lseg = lseg.cpu().numpy()
         Qr, Kr, Vr = (O.bf16_round(x) for x in (Q, K, V))

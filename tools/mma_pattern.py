@@ -4,7 +4,7 @@ import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2512_14082_b200 as us
-L = us.api.lib()
+L = us.api.calib_lib()
 L.us_selftest_mma_pattern.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
 out = torch.zeros(148, dtype=torch.int64, device="cuda")
 names = {0: "transposed: 8 SS N64 K-major -> acc0, 8 SS N64 MN-major -> acc1",

@@ -4,7 +4,7 @@ import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2512_14082_b200 as us
-L = us.api.lib()
+L = us.api.calib_lib()
 L.us_selftest_softmax_probe.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 for threads in (128, 256):
