@@ -342,6 +342,9 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=8, help="KV-head chunks of the pipelined host-buffer path")
     ap.add_argument("--batch", type=int, default=1, help="batch items per layer (partitioned with the heads)")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity sample")
+    ap.add_argument("--also-gain", type=float, nargs="*", default=None,
+                    help="secondary operating points (planted gain) timed on the device path beside the "
+                         "headline (default: 8.0 for C3, the survey's rho ~0.6-0.7 point)")
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -571,6 +574,51 @@ def main():
             log("flashinfer unavailable:", e)
     fastest = min(dense.items(), key=lambda kv: kv[1]) if dense else None
 
+    # ---------------------------------------------------------------- parity record (rank 0, untimed)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = parity_sample(Q, K, V, eng, mode, sel, P)
+        except Exception as e:  # noqa: BLE001 - report, never hide
+            parity = {"error": repr(e)}
+
+    # ---------------------------------------------------------------- secondary operating points
+    # (same shape, other sparsity: the headline gain is the config default; SURVEY §8d
+    # asks for C3 at rho ~0.6-0.7 too — gain 8). Device path only, same timing protocol.
+    extra_gains = args.also_gain if args.also_gain is not None else ([8.0] if args.config == "C3" and gain != 8.0 else [])
+    secondary = []
+    if extra_gains:
+        del eng
+        torch.cuda.empty_cache()
+    for g2 in extra_gains:
+        Q2, K2, V2 = workloads.planted_blocks(L, H, H_kv, d, 64, seed=args.seed, gain=g2, heads=heads, B=args.batch,
+                                              batches=list(shard.batch))
+        e2 = us.Engine(Q2, K2, V2, cfg, head0=shard.q_heads.start)
+        for _ in range(max(args.warmup, 1)):
+            e2.run()
+        torch.cuda.synchronize()
+        sel2 = int(e2.sel.counts.to(torch.int64).sum().item())
+        us.api.profile_enable(args.steps)
+        barrier()
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        for _ in range(args.steps):
+            e2.run()
+        b_.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms2 = max_over_ranks(a_.elapsed_time(b_) / args.steps)
+        st2 = us.api.profile_read(args.steps)
+        us.api.profile_disable()
+        stage2 = {k: statistics.mean(x[k] for x in st2) for k in us.api.STAGES}
+        f2 = sel2 * 4 * 64 * 64 * d / (stage2["attention"] * 1e-3) / 1e12
+        secondary.append({"gain": g2, "rho": 1.0 - sel2 / causal, "ms_per_layer": ms2, "stages_ms": stage2,
+                          "attention_tflops": f2, "attention_frac": f2 / peaks()[2],
+                          "speedup_vs_fastest_dense": (fastest[1] / ms2) if fastest else None})
+        del e2, Q2, K2, V2
+        torch.cuda.empty_cache()
+
     # ---------------------------------------------------------------- roofline of the dominant kernel
     hbm, tf_burst, tf_sust, peak_src = peaks()
     flops_attn = selected * 4 * 64 * 64 * d
@@ -625,12 +673,6 @@ def main():
         if dist:
             dist.destroy_process_group()
         return
-    parity = None
-    if not args.no_parity:
-        try:
-            parity = parity_sample(Q, K, V, eng, mode, sel, P)
-        except Exception as e:  # noqa: BLE001 - report, never hide
-            parity = {"error": repr(e)}
     cpu = None
     if world == 1 and not args.no_cpu:
         v, cores, sample, info = cpu_sample(args.config, gain, P)
@@ -646,7 +688,7 @@ def main():
                roofline=roof, cpu_baseline=cpu,
                stages_ms=stage_ms, stage_roofline=stage_roofs,
                sparsity={"rho": rho, "selected_blocks": selected, "causal_blocks": causal, "attn_tiles": tile_eff},
-               dense_baselines_ms=dense, verify_gather=gather, parity=parity,
+               dense_baselines_ms=dense, verify_gather=gather, parity=parity, secondary_operating_points=secondary,
                speedup_vs_dense={"vs": fastest[0], "dense_ms": fastest[1], "speedup": fastest[1] / ms} if fastest else None)
     print(json.dumps(out), flush=True)
     if dist:

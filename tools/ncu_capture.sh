@@ -9,14 +9,14 @@ L=${2:-131072}; H=${3:-32}; HKV=${4:-8}; GAIN=${5:-9.0}; P=${6:-0.95}
 mkdir -p gpurun_out
 # 1. launch list of one bench step (cold-cache, serialised): per-kernel SHARE of the step
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    -k regex:'attn_kernel|proxy_kernel|compress_kernel|split_kernel|select|mask_check|finalize' \
+    -k regex:'attn_kernel|proxy_kernel|compress_kernel|split_kernel|select|mask_check|finalize|f32_to_bf16|mask_expand' \
     --log-file gpurun_out/ncu_${TAG}_launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu --no-dense > gpurun_out/ncu_${TAG}_bench_under_ncu.log 2>&1
+    python bench.py --steps 2 --warmup 1 --no-cpu --no-dense --no-parity --also-gain > gpurun_out/ncu_${TAG}_bench_under_ncu.log 2>&1
 # 2. full sets: attention (dominant), proxy passes 1+2, compress/split/select
 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 1 -c 1 \
     -o gpurun_out/ncu_${TAG}_attn python tools/profile_case.py $L $H $HKV $GAIN $P > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:proxy -s 2 -c 2 \
     -o gpurun_out/ncu_${TAG}_proxy python tools/profile_case.py $L $H $HKV $GAIN $P > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:'compress_kernel|split_kernel|select_kernel' -s 5 -c 5 \
+ncu --set full --clock-control none --import-source on -k regex:'compress_kernel|split_kernel|select_fused_kernel' -s 4 -c 4 \
     -o gpurun_out/ncu_${TAG}_small python tools/profile_case.py $L $H $HKV $GAIN $P > /dev/null 2>&1
 ls -la gpurun_out/ | grep ncu_${TAG}
