@@ -446,6 +446,15 @@ def main():
     causal = len(shard.batch) * len(heads) * N * (N + 1) // 2
     rho = 1.0 - selected / causal
 
+    # ---------------------------------------------------------------- parity record (rank 0, untimed)
+    # (on the warm-up output: the e2e and dense-baseline legs below overwrite eng.O)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = parity_sample(Q, K, V, eng, mode, sel, P)
+        except Exception as e:  # noqa: BLE001 - report, never hide
+            parity = {"error": repr(e)}
+
     # ---------------------------------------------------------------- timed region (device)
     stream = torch.cuda.current_stream()
     us.api.profile_enable(args.steps)
@@ -573,14 +582,6 @@ def main():
         except Exception as e:  # pragma: no cover
             log("flashinfer unavailable:", e)
     fastest = min(dense.items(), key=lambda kv: kv[1]) if dense else None
-
-    # ---------------------------------------------------------------- parity record (rank 0, untimed)
-    parity = None
-    if rank == 0 and not args.no_parity:
-        try:
-            parity = parity_sample(Q, K, V, eng, mode, sel, P)
-        except Exception as e:  # noqa: BLE001 - report, never hide
-            parity = {"error": repr(e)}
 
     # ---------------------------------------------------------------- secondary operating points
     # (same shape, other sparsity: the headline gain is the config default; SURVEY §8d
