@@ -427,6 +427,24 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
         }
       }
     }
+    // prefetch the partials of this CTA's NEXT row into L2 while this row is selected
+    // (rows are read once from DRAM; the selection phases issue no loads)
+    {
+      const long long rn = rr + gridDim.x;
+      if (rn < sa.rows) {
+        const int plane2 = int(rn % planes), i2 = N - 1 - int(rn / planes);
+        const int nt = ((i2 + 1) * pa.rk + kProxyKeys - 1) / kProxyKeys;  // key tiles holding j <= i2
+        const int ns = kProxyKeys / pa.sw;                                   // slots per key tile
+        const int lines = (rq * ns * 4 + 127) / 128;                          // 128-B lines of one tile's partials
+        for (int e = tid; e < nt * (lines + 1); e += kFusedThreads) {
+          const int t = e / (lines + 1), u = e % (lines + 1);
+          const long long base = ((long long)plane2 * pa.T + t) * pa.Lq + (long long)i2 * rq;
+          const char* ptr = u < lines ? reinterpret_cast<const char*>(pa.part + base * ns) + u * 128
+                                      : reinterpret_cast<const char*>(pa.tmax + base);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+        }
+      }
+    }
     bad = __syncthreads_or(bad);
     nonfinite = __syncthreads_or(nonfinite);
     if (bad && tid == 0) atomicOr(sa.err, 1u);
