@@ -299,19 +299,19 @@ def test_attention_impls_agree(H, H_kv, d):
     mask[..., np.arange(N), np.arange(N)] = True
     bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
     with us().api.calibration() as lib:  # the variants live in the calibration build
-      try:
-        for impl in ((4, 3, 2, 1) if d == 128 else (3, 2, 1)):
-            assert lib.us_set_attention_impl(impl) == 0
-            Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
-            Og = Og.float().cpu().numpy()
-            lseg = lseg.cpu().numpy()
-            for b in range(B):
-                Or, lser = O.block_sparse_attention(Q[b], K[b], V[b], mask[b], 64)
-                assert np.abs(Og[b] - Or).max() <= ATOL, (impl, b)
-                assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO, (impl, b)
-                assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
-      finally:
-        lib.us_set_attention_impl(0)
+        try:
+            for impl in ((4, 3, 2, 1) if d == 128 else (3, 2, 1)):
+                assert lib.us_set_attention_impl(impl) == 0
+                Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
+                Og = Og.float().cpu().numpy()
+                lseg = lseg.cpu().numpy()
+                for b in range(B):
+                    Or, lser = O.block_sparse_attention(Q[b], K[b], V[b], mask[b], 64)
+                    assert np.abs(Og[b] - Or).max() <= ATOL, (impl, b)
+                    assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO, (impl, b)
+                    assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
+        finally:
+            lib.us_set_attention_impl(0)
 
 
 def test_product_library_has_no_calibration_variants():

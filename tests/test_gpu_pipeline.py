@@ -312,3 +312,21 @@ def test_block_size_above_64_matches_oracle(S, d, mode, c):
     O2, _ = us().block_sparse_attention(to_dev_bf16(Q, 1), to_dev_bf16(K, 1), to_dev_bf16(V, 1),
                                         res.report.mask.mask_bits, heads_per_plane=1, S=S)
     assert torch.equal(O2, res.O)
+
+
+@pytest.mark.parametrize("strategy,c_h", [(0, 1), (2, 2)])
+def test_batch_items_equal_single_item_calls(strategy, c_h):
+    """Batch (the north star's B dimension): a B = 3 layer equals three B = 1 calls on
+    its items bit for bit — masks, outputs, lse — for mean and stochastic pooling."""
+    L, H, H_kv, d = 2048, 4, 2, 128
+    items = [workload(O.WL_PLANTED, L, H, H_kv, d, 500 + b) for b in range(3)]
+    cfg = us().CompressionConfig(P=0.95, strategy=strategy, c_h=c_h, seed=9)
+    Qb = torch.stack([to_dev_bf16(it[0], 1)[0] for it in items]).contiguous()
+    Kb = torch.stack([to_dev_bf16(it[1], 1)[0] for it in items]).contiguous()
+    Vb = torch.stack([to_dev_bf16(it[2], 1)[0] for it in items]).contiguous()
+    rb = us().unisparse_attn(Qb, Kb, Vb, cfg)
+    for b in range(3):
+        r1 = us().unisparse_attn(Qb[b:b + 1].contiguous(), Kb[b:b + 1].contiguous(), Vb[b:b + 1].contiguous(), cfg)
+        assert torch.equal(rb.report.mask.mask_bits[b], r1.report.mask.mask_bits[0])
+        assert torch.equal(rb.O[b], r1.O[0])
+        assert torch.equal(rb.lse[b], r1.lse[0])
