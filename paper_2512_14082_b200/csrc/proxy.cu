@@ -309,9 +309,17 @@ __global__ void __launch_bounds__(256) proxy_finalize_kernel(const ProxyArgs a) 
   const int rq = RQ > 0 ? RQ : a.rq;
   if (threadIdx.x < rq) lse_sh[threadIdx.x] = a.lse2[(long long)plane * a.Lq + i * rq + threadIdx.x];
   __syncthreads();
+  constexpr bool kFac = RQ > 0 && SPB > 0;
+  __shared__ float fac[kFac ? 256 * (RQ > 0 ? RQ : 1) : 1];
+  if (kFac) {
+    proxy_tile_factors<(RQ > 0 ? RQ : 1)>(a, plane, i, lse_sh, fac, proxy_tiles_for_row(a, i), threadIdx.x, blockDim.x);
+    __syncthreads();
+  }
   float* out = a.scores + ((long long)plane * a.N + i) * a.N;
   for (int j = threadIdx.x; j <= i; j += blockDim.x) {
-    const float acc = proxy_block_score<SW, RQ, SPB>(a, plane, i, j, lse_sh);
+    float acc;
+    if constexpr (kFac) acc = proxy_block_score_fac<SW, (RQ > 0 ? RQ : 1), (SPB > 0 ? SPB : 1)>(a, plane, i, j, fac);
+    else acc = proxy_block_score<SW, RQ, SPB>(a, plane, i, j, lse_sh);
     out[j] = a.accumulate ? out[j] + acc : acc;
   }
 }

@@ -51,4 +51,43 @@ __device__ __forceinline__ float proxy_block_score(const ProxyArgs& a, int plane
   return acc;
 }
 
+// The c = 8 fast path with per-(key tile, row) factors precomputed once per query
+// block: fac[t * RQ + r] = 2^(m_t(r) - lse2(r)) (0 for a row with no live key), so a
+// score costs RQ partial loads and RQ multiply-adds instead of RQ tile-max loads and
+// exponentials more. Explicit _rn operations (no contraction): every kernel that
+// evaluates a score gets the identical f32 value.
+template <int RQ>
+__device__ __forceinline__ void proxy_tile_factors(const ProxyArgs& a, int plane, int i, const float* lse_sh,
+                                                   float* fac, int n_tiles, int tid, int nthreads) {
+  for (int e = tid; e < n_tiles * RQ; e += nthreads) {
+    const int t = e / RQ, r = e % RQ;
+    const float l = lse_sh[r];
+    fac[e] = l == -INFINITY ? 0.f
+                            : ex2_approx(__ldg(a.tmax + ((long long)plane * a.T + t) * a.Lq + (long long)i * RQ + r) - l);
+  }
+}
+template <int SW, int RQ, int SPB>
+__device__ __forceinline__ float proxy_block_score_fac(const ProxyArgs& a, int plane, int i, int j, const float* fac) {
+  constexpr int NS = kProxyKeys / SW;
+  const int key0 = j * a.rk;
+  const int t = key0 / kProxyKeys, s0 = (key0 % kProxyKeys) / SW;
+  const long long base = ((long long)plane * a.T + t) * a.Lq + (long long)i * RQ;
+  float ps[RQ];
+#pragma unroll
+  for (int r = 0; r < RQ; ++r) {
+    float v = 0.f;
+#pragma unroll
+    for (int u = 0; u < SPB; ++u) v = __fadd_rn(v, __ldg(a.part + (base + r) * NS + s0 + u));
+    ps[r] = v;
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r < RQ; ++r) acc = __fadd_rn(acc, __fmul_rn(ps[r], fac[t * RQ + r]));
+  return acc;
+}
+// key tiles holding the key blocks j <= i of query block i
+__device__ __forceinline__ int proxy_tiles_for_row(const ProxyArgs& a, int i) {
+  return ((i + 1) * a.rk + kProxyKeys - 1) / kProxyKeys;
+}
+
 }  // namespace us

@@ -331,6 +331,7 @@ constexpr int kFusedThreads = 128;
 constexpr int kFusedWarps = kFusedThreads / 32;
 constexpr int kFusedMaxW = kFbMaxN / 32;
 constexpr int kRadixBins = 256;
+constexpr int kMaxFacTiles = 256;  // c = 8 fast path: key tiles per row (L/8/128 <= 256 at L <= 256K)
 
 __device__ __forceinline__ double block_sum_f64(double v, double* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
   extern __shared__ __align__(16) uint8_t fsm[];
   float* sc = reinterpret_cast<float*>(fsm);
   uint32_t* hist = reinterpret_cast<uint32_t*>(fsm + size_t(sa.N) * 4);
+  float* fac_sh = reinterpret_cast<float*>(hist + kRadixBins);  // [key tiles][RQ] (c = 8 fast path)
   __shared__ float lse_sh[128];
   __shared__ double dsh[kFusedWarps];
   __shared__ int ish[kFusedWarps];
@@ -400,16 +402,25 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
     const int n = i + 1;
     if (tid < rq) lse_sh[tid] = pa.lse2[(long long)plane * pa.Lq + (long long)i * rq + tid];
     __syncthreads();
+    constexpr bool kFac = RQ > 0 && SPB > 0;  // c = 8 fast path: per-(tile, row) factors in smem
+    if (kFac) {
+      proxy_tile_factors<(RQ > 0 ? RQ : 1)>(pa, plane, i, lse_sh, fac_sh, proxy_tiles_for_row(pa, i), tid,
+                                           kFusedThreads);
+      __syncthreads();
+    }
     // ---- scores of the row (raw values to sa.scores_out when requested)
     double part = 0.0;
     bool bad = false, nonfinite = false;
-    // four scores per thread in flight (their 4 x 16 partial loads issued together);
+    // four scores per thread in flight (their partial loads issued together);
     // indices past the row are clamped for the loads and discarded
     for (int j0 = tid; j0 < n; j0 += 4 * kFusedThreads) {
       float fv[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) fv[u] = proxy_block_score<SW, RQ, SPB>(pa, plane, i, min(j0 + u * kFusedThreads, n - 1),
-                                                                          lse_sh);
+      for (int u = 0; u < 4; ++u) {
+        const int jj = min(j0 + u * kFusedThreads, n - 1);
+        if constexpr (kFac) fv[u] = proxy_block_score_fac<SW, (RQ > 0 ? RQ : 1), (SPB > 0 ? SPB : 1)>(pa, plane, i, jj, fac_sh);
+        else fv[u] = proxy_block_score<SW, RQ, SPB>(pa, plane, i, jj, lse_sh);
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int j = j0 + u * kFusedThreads;
@@ -643,6 +654,7 @@ __global__ void __launch_bounds__(256) select_fallback_fused_kernel(const ProxyA
   __shared__ unsigned long long keys[kFbMaxN];
   __shared__ uint8_t flag[kFbMaxN];
   __shared__ float lse_sh[128];
+  __shared__ float fac_fb[kMaxFacTiles * 8];
   __shared__ int sh_k;
   __shared__ double sh_cov;
   const int count = *a.fb_count;
@@ -652,11 +664,19 @@ __global__ void __launch_bounds__(256) select_fallback_fused_kernel(const ProxyA
     const int plane = int(row / a.N), i = int(row % a.N), n = i + 1;
     if (threadIdx.x < rq) lse_sh[threadIdx.x] = pa.lse2[(long long)plane * pa.Lq + (long long)i * rq + threadIdx.x];
     __syncthreads();
+    constexpr bool kFac = RQ > 0 && SPB > 0;
+    if (kFac) {
+      proxy_tile_factors<(RQ > 0 ? RQ : 1)>(pa, plane, i, lse_sh, fac_fb, proxy_tiles_for_row(pa, i), threadIdx.x,
+                                           blockDim.x);
+      __syncthreads();
+    }
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
     for (int t = threadIdx.x; t < n2; t += blockDim.x) {
       if (t < n) {
-        float f = proxy_block_score<SW, RQ, SPB>(pa, plane, i, t, lse_sh);
+        float f;
+        if constexpr (kFac) f = proxy_block_score_fac<SW, (RQ > 0 ? RQ : 1), (SPB > 0 ? SPB : 1)>(pa, plane, i, t, fac_fb);
+        else f = proxy_block_score<SW, RQ, SPB>(pa, plane, i, t, lse_sh);
         if (!(f >= 0.f) || f == 0.f) f = 0.f;
         keys[t] = ((unsigned long long)(~__float_as_uint(f)) << 32) | unsigned(t);
       } else {
@@ -733,7 +753,8 @@ __global__ void __launch_bounds__(256) select_fallback_fused_kernel(const ProxyA
 
 template <int SW, int RQ, int SPB>
 void launch_fused_t(const ProxyArgs& pa, const SelectArgs& sa, cudaStream_t st) {
-  const int smem = sa.N * 4 + kRadixBins * 4;  // <= 24 KB (no attribute needed)
+  // scores + bins + the per-(tile, row) factors of the c = 8 path: <= 25 KB (no attribute needed)
+  const int smem = sa.N * 4 + kRadixBins * 4 + (RQ > 0 && SPB > 0 ? kMaxFacTiles * RQ * 4 : 0);
   long long blocks = sa.rows;
   if (blocks > 148 * 16) blocks = 148 * 16;
   select_fused_kernel<SW, RQ, SPB><<<unsigned(blocks), kFusedThreads, smem, st>>>(pa, sa);
