@@ -75,7 +75,9 @@ def test_masks_bit_exact_vs_reference(L, H, H_kv, d, P, mode, c_h, seed):
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, f"mask_flips_L{L}_H{H}_P{P}_m{mode}_ch{c_h}.json"), "w") as f:
         json.dump({"decisions": int(H * N * (N + 1) // 2), "flips": int(len(flips)), "listed": listed}, f, indent=1)
-    assert len(flips) == 0 or all(x["mass_margin_rel"] < 1e-4 or x["score_gap_rel"] < 1e-4 for x in listed), listed
+    # a flip is only admissible at a genuine near-tie of the fp64 rule (the fp32-class
+    # proxy moves scores by ~1e-7 relative); every flip is listed with its margins
+    assert len(flips) == 0 or all(x["mass_margin_rel"] < 1e-6 or x["score_gap_rel"] < 1e-6 for x in listed), listed
     assert len(flips) <= max(2, H * N * (N + 1) // 2 // 20000), f"{len(flips)} flipped blocks: {listed[:5]}"
 
 
@@ -279,7 +281,12 @@ def test_fuzz_pipeline_against_oracle(case):
     rel = np.abs(g_scores - r_scores)[:, tri][big] / r_scores[:, tri][big]
     assert rel.max() < 1e-3, rel.max()
     ref_mask, _ = O.build_block_mask(r_scores, H, c["c_h"], c["P"], select_mode=sel, top_k=c["topk"])
-    assert int((ref_mask != g_mask).sum()) <= max(2, H * N * (N + 1) // 2 // 20000)
+    flips = np.argwhere(ref_mask != g_mask)
+    assert len(flips) <= max(2, H * N * (N + 1) // 2 // 20000)
+    # every flip vs the fp64 rule must sit at a near-tie (listed with its margins)
+    margins = [dict(head=int(h), **mask_margins(r_scores[h // c["c_h"]], c["P"] if not c["topk"] else 1.0, int(i), int(j)))
+               for h, i, j in flips]
+    assert all(m["mass_margin_rel"] < 1e-6 or m["score_gap_rel"] < 1e-6 for m in margins), margins
     Og = res.O.float().cpu().numpy()[0]
     Or, _ = O.block_sparse_attention(Q, K, V, g_mask, 64)
     assert np.abs(Og - Or).max() <= 1e-2 * np.abs(Or).max() + 1e-4
