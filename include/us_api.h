@@ -227,7 +227,9 @@ us_status us_selection_flops(const us_params* p, int32_t proxy, int32_t stride, 
  * 0 = automatic (default, = 1); 1 = attention.cu (two M=128 query tiles per CTA, 64-key steps),
  * 2 = attention2.cu (one tile per CTA, 128-key steps), 3 = attention.cu with one
  * tile (two query groups) per CTA and two CTAs per SM, 4 = attention_kt.cu (key
- * blocks as the MMA M dimension, one query group per work item; d_k = 128). All compute the same function; the environment variable
+ * blocks as the MMA M dimension, one query group per work item; d_k = 128), 5 = attention_tp.cu
+ * (P in TMEM, two logit buffers per tile, Q in SMEM, split K / V rings). 2-5 exist only in the
+ * calibration build. All compute the same function; the environment variable
  * US_ATTN_IMPL sets the initial choice. */
 us_status us_set_attention_impl(int32_t impl);
 

@@ -155,7 +155,7 @@ _calib = None
 
 def calib_lib() -> C.CDLL:
     """The calibration build (-DUS_CALIBRATION): the product plus the measured-slower
-    attention variants (us_set_attention_impl 2-4) and the hardware probes
+    attention variants (us_set_attention_impl 2-5) and the hardware probes
     (us_selftest_*). Loaded separately (RTLD_LOCAL), never the default path."""
     global _calib
     with _lib_lock:

@@ -2,8 +2,9 @@
   paper_2512_14082_b200/_build/libunisparse_b200.so        the product (the hot path + the C ABI)
   paper_2512_14082_b200/_build/libunisparse_b200_calib.so  calibration build (-DUS_CALIBRATION):
       the product plus the measured-slower attention variants (attention2.cu, the one-tile
-      attention.cu instantiation, the key-major attention_kt.cu) and the tcgen05 / TMEM /
-      MUFU probes (selftest.cu) — for tests/tools that select them, never the default path.
+      attention.cu instantiation, the key-major attention_kt.cu, the decoupled-softmax
+      attention_tp.cu) and the tcgen05 / TMEM / MUFU probes (selftest.cu) — for tests/tools
+      that select them, never the default path.
 
 nvcc cross-compiles without a GPU; the .so travels to the GPU box with the
 repo snapshot (git-ignored, not gpurun-ignored).
@@ -21,7 +22,7 @@ CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "libunisparse_b200.so")
 SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "lastblock.cu", "io.cu", "metrics.cu"]
-CALIB_SOURCES = SOURCES + ["attention2.cu", "attention_kt.cu", "selftest.cu"]
+CALIB_SOURCES = SOURCES + ["attention2.cu", "attention_kt.cu", "attention_tp.cu", "selftest.cu"]
 CALIB_LIB = os.path.join(OUT_DIR, "libunisparse_b200_calib.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

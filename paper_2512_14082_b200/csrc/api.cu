@@ -415,13 +415,14 @@ us_status run_select_fused(const us_params& p, const ProxyArgs& pa, uint32_t* ma
 // (default: the key-major attention_kt.cu for block-sparse masks at d_k = 128,
 // attention.cu for dense / d_k = 64), 1 = attention.cu (two M=128 query tiles
 // per CTA, 64-key steps), 2 = attention2.cu, 3 = attention.cu with one tile per
-// CTA, 4 = attention_kt.cu whenever d_k = 128 (dense included).
+// CTA, 4 = attention_kt.cu whenever d_k = 128 (dense included), 5 = attention_tp.cu
+// (decoupled softmax: P in TMEM, two logit buffers per tile). 2-5: calibration build only.
 std::atomic<int> g_attn_impl{-1};
 int attention_impl() {
   int v = g_attn_impl.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = std::getenv("US_ATTN_IMPL");
-    v = (e && std::atoi(e) >= 1 && std::atoi(e) <= 4) ? std::atoi(e) : 0;
+    v = (e && std::atoi(e) >= 1 && std::atoi(e) <= 5) ? std::atoi(e) : 0;
     g_attn_impl.store(v, std::memory_order_relaxed);
   }
   return v;
@@ -482,6 +483,7 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   }
   if (impl == 2 && !a.noncausal) return launch_attention2(a, tK, tV, st);
   a.one_tile = impl == 3 ? 1 : 0;
+  if (impl == 5) return launch_attention_tp(a, tQ, tK3, tV3, st);
 #else
   (void)impl;
 #endif
@@ -609,14 +611,14 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
 us_status us_set_attention_impl(int32_t impl) {
 #ifndef US_CALIBRATION
   if (impl >= 2) {
-    set_error("us_set_attention_impl: implementations 2-4 are calibration variants, present only in "
+    set_error("us_set_attention_impl: implementations 2-5 are calibration variants, present only in "
               "libunisparse_b200_calib.so");
     return US_ERR_UNSUPPORTED;
   }
 #endif
-  if (impl < 0 || impl > 4) {
+  if (impl < 0 || impl > 5) {
     set_error("us_set_attention_impl: impl must be 0 (automatic), 1 (two query tiles per CTA), 2 (128-key steps), "
-              "3 (one tile per CTA) or 4 (key-major)");
+              "3 (one tile per CTA), 4 (key-major) or 5 (decoupled softmax, P in TMEM)");
     return US_ERR_INVALID_ARGUMENT;
   }
   g_attn_impl.store(impl, std::memory_order_relaxed);

@@ -43,6 +43,7 @@
 #include "host_util.hpp"
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "attn_common.cuh"
 
 #ifndef US_ATTN_SKELETON
 #define US_ATTN_SKELETON 0
@@ -77,9 +78,12 @@ __device__ int g_attn_trace_cta;
 namespace us {
 namespace {
 
-constexpr int kBS = 64;     // block size (keys per tile, rows per group)
-constexpr int kMaxN = 4096; // blocks per row
-constexpr int kMaxW = kMaxN / 32;
+using attn::kBS;
+using attn::kMaxN;
+using attn::kMaxW;
+using attn::Groups;
+using attn::decode_item;
+using attn::ex2_poly2;
 
 // K/V ring depth: a 64-key K+V tile takes ~1-2 us to land from L2, so the ring
 // must cover several steps of prefetch.
@@ -101,78 +105,11 @@ struct AttnSmem {
 // TMEM columns of tile X start at X * 256: S [0,64), O [64, 64+D), Q [192, 192+D/2).
 constexpr uint32_t kTS = 0, kTO = 64, kTQ = 192;
 
-// exp2 on the FMA/ALU pipes for a pair of values (offloads MUFU): round-to-nearest
-// split x = n + f, f in [-0.5, 0.5], cubic minimax for 2^f (max rel. err 7.7e-5,
-// far below the bf16 rounding of P), exponent added in the integer domain. x <= 8.
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -125.0f);
-  x.y = fmaxf(x.y, -125.0f);
-  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));  // 1.5 * 2^23
-  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
-  float2 p = __ffma2_rn(make_float2(0.05508868396282196f, 0.05508868396282196f), f,
-                        make_float2(0.24260404706001282f, 0.24260404706001282f));
-  p = __ffma2_rn(p, f, make_float2(0.6932762265205383f, 0.6932762265205383f));
-  p = __ffma2_rn(p, f, make_float2(0.9999289512634277f, 0.9999289512634277f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-
 #ifndef US_ATTN_POLY_FROM
 #define US_ATTN_POLY_FROM 56
 #endif
 // columns [kPolyFrom, 64) of an off-diagonal tile use ex2_poly2 (FMA pipe)
 constexpr int kPolyFrom = US_ATTN_POLY_FROM;
-
-// Work order: KV head outermost, query blocks heaviest-first inside it, so the
-// ~148 resident CTAs all stream K/V of ONE KV head (L * d * 4 bytes = 64 MB at
-// 128K, d=128) and their random selected-block reads hit the 126 MB L2. The
-// earlier query-block-major order spread them over every KV head (the whole
-// 512 MB K/V) and ncu measured 130 GB of DRAM reads per layer (r01 profile).
-struct Groups {
-  int b, h[4], i[4];
-  bool en[4];
-};
-
-__device__ __forceinline__ Groups decode_item(const AttnArgs& a, int item) {
-  Groups g;
-  const int G = a.H / a.H_kv;
-  if (a.group_mode == 0) {  // 4 heads of a KV group, one query block
-    const int quads = a.H / 4;
-    const int i = a.N - 1 - item % a.N;
-    const int bq = item / a.N;
-    g.b = bq / quads;
-    const int h0 = (bq % quads) * 4;
-    for (int k = 0; k < 4; ++k) {
-      g.h[k] = h0 + k;
-      g.i[k] = i;
-      g.en[k] = true;
-    }
-  } else if (a.group_mode == 1) {  // 2 heads x query blocks (i, i-1)
-    const int npairs = (a.N + 1) / 2;
-    const int ip = npairs - 1 - item % npairs;
-    const int bk = item / npairs;
-    g.b = bk / a.H_kv;
-    const int h0 = (bk % a.H_kv) * G;
-    const int ib = 2 * ip + 1, ia = 2 * ip;
-    for (int k = 0; k < 4; ++k) {
-      g.h[k] = h0 + (k & 1);
-      g.i[k] = k < 2 ? ib : ia;
-    }
-    for (int k = 0; k < 4; ++k) g.en[k] = g.i[k] < a.N;
-  } else {  // one head, 4 query blocks
-    const int nq = (a.N + 3) / 4;
-    const int iq = nq - 1 - item % nq;
-    const int bh = item / nq;
-    g.b = bh / a.H;
-    for (int k = 0; k < 4; ++k) {
-      g.h[k] = bh % a.H;
-      g.i[k] = 4 * iq + 3 - k;
-      g.en[k] = g.i[k] < a.N;
-    }
-  }
-  return g;
-}
 
 // One-tile CTAs: two groups that read the same KV head — two heads of a KV group at
 // one query block (G even) or one head at query blocks (i, i-1) (G odd); groups 2, 3
@@ -218,14 +155,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
   __shared__ uint64_t bar_q[2], bar_kvfull[kST], bar_kvempty[kST], bar_sfull[2], bar_sfree[2], bar_pfull[2],
       bar_pvdone[2], bar_ofull[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int n_steps_sh;
-  __shared__ uint32_t perm_sh;  // group of tile slot s = (perm_sh >> 2s) & 3
-  __shared__ uint32_t mrow[4][kMaxW];
-  // union of the four groups' selected blocks, ascending: j | sel_slot << (12 + slot)
-  __shared__ uint16_t steps[kMaxN];
-  // per tile: the union positions it computes (its own steps), ascending
-  __shared__ uint16_t own_pos[2][kMaxN];
-  __shared__ int n_own_sh[2];
+  __shared__ attn::Lists ls;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if US_ATTN_TRACE
@@ -234,9 +164,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
   const int G = a.H / a.H_kv;
   const Groups gr = NT == 2 ? decode_item(a, blockIdx.x) : decode_pair(a, blockIdx.x);
   const int kvh = gr.h[0] / G;
-  int jmax = -1;
-  for (int k = 0; k < 4; ++k)
-    if (gr.en[k]) jmax = max(jmax, a.noncausal ? a.N - 1 : gr.i[k]);
+  const int jmax = attn::last_block(a, gr);
 
   if (threadIdx.x == 0) {
     for (int x = 0; x < 2; ++x) {
@@ -255,127 +183,12 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, NT * 256);
-  if (warp == 2) {
-    // mask rows restricted to the causal prefix j <= i_g, then the ascending union list
-    const int nw = jmax >= 0 ? (jmax >> 5) + 1 : 0;
-    for (int g = 0; g < 4; ++g) {
-      const int ig = gr.i[g];
-      const uint32_t* src =
-          a.mask ? a.mask + ((long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + ig) * a.W
-                 : nullptr;
-      // (non-causal dense attention, dense_attention(in, false): every key block j < N)
-      const int jlast = a.noncausal ? a.N - 1 : ig;
-      for (int w = lane; w < nw; w += 32) {
-        uint32_t word = 0;
-        if (gr.en[g] && (w << 5) <= jlast) {
-          word = src ? src[w] : ~0u;
-          const int hi = jlast - (w << 5);  // bits 0..hi are attended
-          if (hi < 31) word &= (2u << hi) - 1u;
-        }
-        mrow[g][w] = word;
-      }
-    }
-    __syncwarp();
-    if (a.err && a.mask) {
-      // asynchronous data-error report (the reference throws, attention.cpp:106-108,
-      // 127-129): a non-causal bit anywhere in a group's row, or an empty causal prefix
-      for (int g = 0; g < 4; ++g) {
-        if (!gr.en[g]) continue;
-        const int ig = gr.i[g];
-        const long long row = (long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + ig;
-        const uint32_t* src = a.mask + row * a.W;
-        uint32_t bad = 0;
-        int cnt = 0;
-        for (int w = lane; w < a.W; w += 32) {
-          const uint32_t word = src[w];
-          const int lo = w << 5;
-          const uint32_t keep = lo > ig ? 0u : (ig - lo >= 31 ? ~0u : (2u << (ig - lo)) - 1u);
-          bad |= word & ~keep;
-          cnt += __popc(word & keep);
-        }
-        bad = __reduce_or_sync(0xffffffffu, bad);
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        if (lane == 0 && (bad || cnt == 0)) {
-          atomicOr(a.err, bad ? 4u : 8u);
-          atomicMin(a.first_bad, int32_t(row));
-        }
-      }
-    }
-    // Pair the four groups into the two tiles so that the LONGER tile's step count
-    // (its pair's union) is smallest: the CTA lasts as long as its longer tile, and
-    // the per-head selection sizes differ (tools/tile_pairing.py: -11 % on the sum
-    // of the longer tiles at C3, +1 % tile steps). Ties keep the natural order.
-    int c01 = 0, c23 = 0, c02 = 0, c13 = 0, c03 = 0, c12 = 0;
-    for (int w = lane; w < nw; w += 32) {
-      const uint32_t m0 = mrow[0][w], m1 = mrow[1][w], m2 = mrow[2][w], m3 = mrow[3][w];
-      c01 += __popc(m0 | m1);
-      c23 += __popc(m2 | m3);
-      c02 += __popc(m0 | m2);
-      c13 += __popc(m1 | m3);
-      c03 += __popc(m0 | m3);
-      c12 += __popc(m1 | m2);
-    }
-    c01 = __reduce_add_sync(0xffffffffu, c01);
-    c23 = __reduce_add_sync(0xffffffffu, c23);
-    c02 = __reduce_add_sync(0xffffffffu, c02);
-    c13 = __reduce_add_sync(0xffffffffu, c13);
-    c03 = __reduce_add_sync(0xffffffffu, c03);
-    c12 = __reduce_add_sync(0xffffffffu, c12);
-    int pr = 0, best = max(c01, c23) * 4096 + c01 + c23;
-    const int k1 = max(c02, c13) * 4096 + c02 + c13, k2 = max(c03, c12) * 4096 + c03 + c12;
-    if (NT == 2 && a.pairing && k1 < best) { pr = 1; best = k1; }
-    if (NT == 2 && a.pairing && k2 < best) { pr = 2; best = k2; }
-    // slot s (tile s / 2, rows (s & 1) * 64 ..) holds group perm[s]
-    const uint32_t perm = pr == 0 ? 0xE4u : pr == 1 ? 0xD8u : 0x9Cu;  // 2-bit fields: 0123 / 0213 / 0312
-    int base = 0;
-    for (int w0 = 0; w0 < nw; w0 += 32) {
-      const int w = w0 + lane;
-      uint32_t m[4];
-#pragma unroll
-      for (int sl = 0; sl < 4; ++sl) m[sl] = w < nw ? mrow[(perm >> (2 * sl)) & 3u][w] : 0u;
-      uint32_t u = m[0] | m[1] | m[2] | m[3];
-      const int cnt = __popc(u);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int pos = base + incl - cnt;
-      while (u) {
-        const int bit = __ffs(u) - 1;
-        u &= u - 1u;
-        uint32_t e = uint32_t((w << 5) + bit);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) e |= ((m[g] >> bit) & 1u) << (12 + g);
-        steps[pos++] = uint16_t(e);
-      }
-      base += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    __syncwarp();
-    // own-step lists of the two tiles (the softmax warps walk only their own steps)
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-      int n = 0;
-      for (int t0 = 0; t0 < base; t0 += 32) {
-        const int t = t0 + lane;
-        const bool mine = t < base && ((steps[t] >> (12 + 2 * x)) & 3u) != 0u;
-        const uint32_t b = __ballot_sync(0xffffffffu, mine);
-        if (mine) own_pos[x][n + __popc(b & ((1u << lane) - 1u))] = uint16_t(t);
-        n += __popc(b);
-      }
-      if (lane == 0) n_own_sh[x] = n;
-    }
-    if (lane == 0) {
-      n_steps_sh = base;
-      perm_sh = perm;
-    }
-  }
+  if (warp == 2) attn::build_lists(a, gr, jmax, NT == 2 && a.pairing, ls, ls.own_pos);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const int T = n_steps_sh;
+  const int T = ls.n_steps;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -385,7 +198,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       const uint64_t pol_kv = policy_evict_last();
       const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
       for (int t = 0; t < T; ++t) {
-        const int j = int(steps[t] & 0xFFFu);
+        const int j = int(ls.steps[t] & 0xFFFu);
         const int s = t % kST;
         if (t >= kST) mbar_wait(&bar_kvempty[s], ((t / kST) + 1) & 1);
         uint8_t* sk = smem + s * 2 * SL::kKVBytes;
@@ -404,9 +217,9 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
     constexpr uint32_t idesc_o = idesc_f16(128, D, /*bf16*/ 1, false, /*V MN-major*/ true);
     const uint32_t tb = tmem + x * 256;
     const uint32_t sP = smem_u32(smem + SL::kRingBytes + x * SL::kPBytes);
-    const int n_own = n_own_sh[x];
+    const int n_own = ls.n_own[x];
     // union position of own step kk (T past the last)
-    auto own_at = [&](int kk) { return kk < n_own ? int(own_pos[x][kk]) : T; };
+    auto own_at = [&](int kk) { return kk < n_own ? int(ls.own_pos[x][kk]) : T; };
     // Release union positions [from, to) this tile skips. Waiting for each tile to
     // land keeps this warp's kv_empty arrivals in phase order (one per stage phase).
     auto release = [&](int from, int to) {
@@ -478,7 +291,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
     const int q = warp & 3;         // TMEM lane quarter
     const int row = q * 32 + lane;
     const int slot = 2 * x + (row >> 6), rloc = row & 63;
-    const int g = int((perm_sh >> (2 * slot)) & 3u);
+    const int g = int((ls.perm >> (2 * slot)) & 3u);
     const int ig = gr.i[g], hg = gr.h[g];
     const bool en = gr.en[g];
     const uint32_t lane_addr = uint32_t(q * 32) << 16;
@@ -509,9 +322,9 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       if (lane == 0) mbar_arrive(&bar_q[x]);
     }
     int k = 0;
-    const int n_own = n_own_sh[x];
+    const int n_own = ls.n_own[x];
     for (int kk = 0; kk < n_own; ++kk) {
-      const uint32_t e = steps[own_pos[x][kk]];
+      const uint32_t e = ls.steps[ls.own_pos[x][kk]];
       const int j = int(e & 0xFFFu);
       const bool sel = (e >> (12 + slot)) & 1u;
       mbar_wait(&bar_sfull[x], k & 1);

@@ -149,6 +149,13 @@ struct AttnArgs {
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);
 
+// Decoupled-softmax variant (attention_tp.cu): same work decomposition and union lists
+// as launch_attention; two logit buffers per tile in TMEM, P written back into them and
+// P.V as a TS-mode MMA, Q in SMEM (SS-mode S), two softmax warps per lane quarter.
+// tmQ: 2-D map (box 64 rows x 64); tmK / tmV: 3-D rows-chunked maps (box 64 rows).
+us_status launch_attention_tp(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                              const CUtensorMap& tmV, cudaStream_t st);
+
 // Key-major variant (attention_kt.cu, d_k = 128): one query group per work item,
 // M = 128 = a pair of its own selected key blocks (no union rows); persistent CTAs.
 // tmQ3 / tmV3: 3-D rows-chunked maps (box 64 rows), tmK2: 2-D map (box 64 x 64).

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cstdio>
 
 namespace us {
 
@@ -76,7 +77,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if US_WATCHDOG
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > 4000000000ll) __trap();
+    if (clock64() - t0 > 4000000000ll) {
+#ifdef US_WATCHDOG_PRINT
+      printf("watchdog: block %d thread %d smem bar 0x%x parity %u\n", int(blockIdx.x), int(threadIdx.x),
+             smem_u32(bar), parity);
+#endif
+      __trap();
+    }
   }
 #else
   while (!mbar_try_wait(bar, parity)) {

@@ -286,9 +286,11 @@ def test_sparse_attention_rejects_malformed_masks():
 
 @pytest.mark.parametrize("H,H_kv,d", [(8, 4, 128), (4, 4, 64), (6, 2, 128), (3, 1, 128)])
 def test_attention_impls_agree(H, H_kv, d):
-    """attention.cu (64-key steps, two tiles per CTA) and attention2.cu (128-key
-    steps, one tile per CTA) on the same random masks — odd union lengths
-    included: both equal the fp64 oracle within the bf16 tolerance."""
+    """attention.cu (64-key steps, two tiles per CTA) and the calibration variants —
+    attention2.cu (128-key steps, one tile per CTA), the one-tile attention.cu, the
+    key-major attention_kt.cu and the decoupled-softmax attention_tp.cu (P in TMEM,
+    double-buffered logits, split K / V rings) — on the same random masks, odd union
+    lengths included: all equal the fp64 oracle within the bf16 tolerance."""
     import ctypes
     rng = np.random.default_rng(H * 100 + d)
     B, L = 2, 1024
@@ -300,7 +302,7 @@ def test_attention_impls_agree(H, H_kv, d):
     bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
     with us().api.calibration() as lib:  # the variants live in the calibration build
         try:
-            for impl in ((4, 3, 2, 1) if d == 128 else (3, 2, 1)):
+            for impl in ((5, 4, 3, 2, 1) if d == 128 else (5, 3, 2, 1)):
                 assert lib.us_set_attention_impl(impl) == 0
                 Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
                 Og = Og.float().cpu().numpy()
@@ -315,11 +317,12 @@ def test_attention_impls_agree(H, H_kv, d):
 
 
 def test_product_library_has_no_calibration_variants():
-    """The product library runs attention.cu only: the calibration variants (2-4) and the
+    """The product library runs attention.cu only: the calibration variants (2-5) and the
     probes are absent from libunisparse_b200.so (they live in the calibration build)."""
     lib = us().api.lib()
     assert lib.us_set_attention_impl(2) == us().api.US_ERR_UNSUPPORTED
     assert lib.us_set_attention_impl(4) == us().api.US_ERR_UNSUPPORTED
+    assert lib.us_set_attention_impl(5) == us().api.US_ERR_UNSUPPORTED
     assert lib.us_set_attention_impl(0) == 0
     assert not hasattr(lib, "us_selftest_umma")
 
