@@ -278,7 +278,9 @@ inline CompressedViews compress(const AttentionInputs& in, const CompressionConf
   const size_t planes = size_t(in.B) * (in.H / cfg.c_h);
   v.Qc = DeviceBuffer<float>(planes * (in.L / cfg.c_q) * in.d_k);
   v.Kc = DeviceBuffer<float>(planes * (in.L / cfg.c_k) * in.d_k);
-  detail::raise(us_compress(&p, in.Q, in.K, v.Qc.data(), v.Kc.data(), nullptr, 0, in.stream));
+  DeviceBuffer<std::uint8_t> ws;  // d_k outside {64, 128}: zero-padded copies in the workspace
+  if (in.d_k != 64 && in.d_k != 128) ws = detail::workspace(p);
+  detail::raise(us_compress(&p, in.Q, in.K, v.Qc.data(), v.Kc.data(), ws.data(), ws.size(), in.stream));
   return v;
 }
 
@@ -376,8 +378,8 @@ inline AttentionOutput dense_attention(const AttentionInputs& in, bool causal = 
   AttentionOutput out;
   out.O = DeviceBuffer<std::uint16_t>(size_t(in.B) * in.H * in.L * in.d_k);
   out.lse = DeviceBuffer<float>(size_t(in.B) * in.H * in.L);
-  DeviceBuffer<std::uint8_t> ws;  // f32 inputs: the bf16 copies live in the workspace
-  if (in.f32) ws = detail::workspace(p);
+  DeviceBuffer<std::uint8_t> ws;  // f32 inputs: bf16 copies; d_k outside {64, 128}: padded copies
+  if (in.f32 || (in.d_k != 64 && in.d_k != 128)) ws = detail::workspace(p);
   detail::raise(us_dense_attention(&p, in.Q, in.K, in.V, out.O.data(), out.lse.data(), ws.data(), ws.size(),
                                    in.stream));
   return out;

@@ -369,7 +369,9 @@ def compress(Q: torch.Tensor, K: torch.Tensor, cfg: CompressionConfig, S: int = 
     Hc = max(H // max(cfg.c_h, 1), 1)
     Qc = torch.empty((B, Hc, L // max(cfg.c_q, 1), d), dtype=torch.float32, device=Q.device)
     Kc = torch.empty((B, Hc, L // max(cfg.c_k, 1), d), dtype=torch.float32, device=Q.device)
-    _raise(lib().us_compress(C.byref(p), _ptr(Q), _ptr(K), _ptr(Qc), _ptr(Kc), None, 0, _stream()))
+    ws = workspace(p) if d not in (64, 128) else None  # other d_k run zero-padded in the workspace
+    _raise(lib().us_compress(C.byref(p), _ptr(Q), _ptr(K), _ptr(Qc), _ptr(Kc), _ptr(ws),
+                             ws.numel() if ws is not None else 0, _stream()))
     return Qc, Kc
 
 
@@ -428,7 +430,8 @@ def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: in
     O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
-    ws = workspace(p) if (validate_mask or Q.dtype == torch.float32 or S != 64) else None
+    ws = workspace(p) if (validate_mask or Q.dtype == torch.float32 or S != 64 or Q.shape[-1] not in (64, 128)) \
+        else None
     _raise(lib().us_sparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(mask_bits.contiguous()),
                                      heads_per_plane, _ptr(O), _ptr(lse), _ptr(ws),
                                      ws.numel() if ws is not None else 0, _stream()))
@@ -463,7 +466,8 @@ def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True, causal: bool = 
     O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
-    ws = workspace(p) if Q.dtype == torch.float32 else None  # f32 inputs: bf16 copies in the workspace
+    # f32 inputs: bf16 copies in the workspace; d_k outside {64, 128}: zero-padded copies
+    ws = workspace(p) if (Q.dtype == torch.float32 or Q.shape[-1] not in (64, 128)) else None
     _raise(lib().us_dense_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse), _ptr(ws),
                                     ws.numel() if ws is not None else 0, _stream()))
     return O, lse

@@ -86,8 +86,8 @@ Checked check(const us_params& p, bool need_compression) {
     e.push_back("unknown causal_mode");
   if (!e.empty()) return c;
   auto& u = c.unsupported;
-  if (p.d_k != 64 && p.d_k != 128)
-    u.push_back("d_k=" + std::to_string(p.d_k) + " unsupported on the GPU path (64 or 128)");
+  if (p.d_k > 128)
+    u.push_back("d_k=" + std::to_string(p.d_k) + " unsupported on the GPU path (at most 128)");
   if (p.S != kGpuBlock && p.S != 2 * kGpuBlock && p.S != 4 * kGpuBlock)
     u.push_back("S=" + std::to_string(p.S) + " unsupported on the GPU path (64, 128 or 256)");
   if (p.L / kGpuBlock > 4096) u.push_back("L/64 above 4096 unsupported on the GPU path");
@@ -126,8 +126,22 @@ us_status gate(const us_params* p, const char* who, bool need_compression) {
 }
 
 // ---------------------------------------------------------------- geometry
+// d_k outside {64, 128} (the reference accepts any d_k, types.hpp:66-72): the entry points
+// stage copies zero-padded to the next supported width in the workspace and run the same
+// kernels at that width (zeros pool to exact zeros and add exact zeros to every dot product,
+// so compressed rows, logits, masks and outputs equal the unpadded computation); the
+// softmax scale keeps the caller's d_k, set for the duration of the inner call here.
+thread_local int t_scale_dk = 0;
+struct ScaleDk {
+  int prev;
+  explicit ScaleDk(int d) : prev(t_scale_dk) { t_scale_dk = d; }
+  ~ScaleDk() { t_scale_dk = prev; }
+};
+int padded_dk(int d) { return d <= 64 ? 64 : 128; }
+bool needs_pad(const us_params& p) { return p.d_k != padded_dk(p.d_k); }
+
 struct Geo {
-  int B, H, H_kv, G, L, D, S, N, W, Hc, Lq, Lk, rq, rk;
+  int B, H, H_kv, G, L, D, Ds, S, N, W, Hc, Lq, Lk, rq, rk;
   bool kv_dedup;
   int kv_planes, kv_mul, kv_div;
   explicit Geo(const us_params& p) {
@@ -137,6 +151,7 @@ struct Geo {
     G = H / H_kv;
     L = p.L;
     D = p.d_k;
+    Ds = t_scale_dk > 0 ? t_scale_dk : p.d_k;  // d_k of the softmax scale 1/sqrt(d_k)
     S = p.S;
     N = L / S;
     W = (N + 31) / 32;
@@ -224,6 +239,84 @@ us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, b
   return US_OK;
 }
 
+// Padded d_k staging (see padded_dk): the inner call's workspace comes first (so the error
+// header sits where us_check_device_errors looks for it), then zero-padded copies of the
+// inputs and of the outputs the call produces at the padded width.
+struct PadWs {
+  size_t q, k, v, o, qc, kc, total;
+};
+PadWs pad_layout(const us_params& p) {
+  Geo g(p);
+  const size_t Dp = size_t(padded_dk(p.d_k)), es = p.dtype == US_DTYPE_F32 ? 4 : 2;
+  PadWs w{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = al(o + bytes);
+    return at;
+  };
+  w.q = take(es * size_t(g.B) * g.H * g.L * Dp);
+  w.k = take(es * size_t(g.B) * g.H_kv * g.L * Dp);
+  w.v = take(es * size_t(g.B) * g.H_kv * g.L * Dp);
+  w.o = take(2 * size_t(g.B) * g.H * g.L * Dp);
+  w.qc = take(4 * size_t(g.B) * g.Hc * g.Lq * Dp);
+  w.kc = take(4 * size_t(g.B) * g.Hc * g.Lk * Dp);
+  w.total = o;
+  return w;
+}
+us_params padded_params(const us_params& p) {
+  us_params q = p;
+  q.d_k = padded_dk(p.d_k);
+  return q;
+}
+size_t padded_ws_bytes(const us_params& p) { return al(layout(padded_params(p)).total) + pad_layout(p).total; }
+
+struct PadStage {
+  us_params pp;        // the same call at the padded width
+  size_t inner_bytes;  // workspace of the inner call, at the start of the caller's
+  uint8_t* base;       // padded copies
+  PadWs w;
+  size_t es;           // bytes per input element
+};
+// inner_total: the inner call's workspace at the padded width (default: layout(pp))
+us_status pad_begin(const us_params& p, void* ws, size_t bytes, const char* who, PadStage& ps,
+                    size_t inner_total = 0) {
+  ps.pp = padded_params(p);
+  ps.inner_bytes = al(inner_total ? inner_total : layout(ps.pp).total);
+  ps.w = pad_layout(p);
+  ps.es = p.dtype == US_DTYPE_F32 ? 4 : 2;
+  const size_t need = ps.inner_bytes + ps.w.total;
+  if (!ws || bytes < need) {
+    set_error(std::string(who) + ": workspace of " + std::to_string(need) + " bytes required (d_k=" +
+              std::to_string(p.d_k) + " runs zero-padded to " + std::to_string(ps.pp.d_k) + ")");
+    return US_ERR_WORKSPACE;
+  }
+  ps.base = static_cast<uint8_t*>(ws) + ps.inner_bytes;
+  return US_OK;
+}
+// rows x d -> rows x Dp with zero columns [d, Dp)
+us_status pad_rows(const void* src, void* dst, size_t rows, int d, int Dp, size_t es, cudaStream_t st) {
+  US_CUDA_TRY(cudaMemcpy2DAsync(dst, Dp * es, src, d * es, d * es, rows, cudaMemcpyDeviceToDevice, st), "d_k pad copy");
+  US_CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(dst) + d * es, Dp * es, 0, (Dp - d) * es, rows, st),
+              "d_k pad clear");
+  return US_OK;
+}
+us_status unpad_rows(const void* src, void* dst, size_t rows, int d, int Dp, size_t es, cudaStream_t st) {
+  US_CUDA_TRY(cudaMemcpy2DAsync(dst, d * es, src, Dp * es, d * es, rows, cudaMemcpyDeviceToDevice, st), "d_k unpad copy");
+  return US_OK;
+}
+// stage Q (and K, V when given) at the padded width
+us_status pad_inputs(const us_params& p, const PadStage& ps, const void* Q, const void* K, const void* V,
+                     cudaStream_t st) {
+  Geo g(p);
+  us_status s;
+  const int Dp = ps.pp.d_k;
+  if (Q && (s = pad_rows(Q, ps.base + ps.w.q, size_t(g.B) * g.H * g.L, g.D, Dp, ps.es, st)) != US_OK) return s;
+  if (K && (s = pad_rows(K, ps.base + ps.w.k, size_t(g.B) * g.H_kv * g.L, g.D, Dp, ps.es, st)) != US_OK) return s;
+  if (V && (s = pad_rows(V, ps.base + ps.w.v, size_t(g.B) * g.H_kv * g.L, g.D, Dp, ps.es, st)) != US_OK) return s;
+  return US_OK;
+}
+
 // compress + split + proxy (logits, row LSE, slot partials). The block scores are
 // formed by the fused selection (launch_select_fused with *pa_out).
 us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, cudaStream_t st,
@@ -278,7 +371,7 @@ us_status run_proxy(const us_params& p, const void* Q, const void* K, void* ws, 
   pa.tmax = at<float>(ws, w.tmax);
   pa.lse2 = at<float>(ws, w.lse2);
   pa.scores = nullptr;
-  pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.Ds)));
   pa.x3 = 1;
   pa.finalize = 0;
   *pa_out = pa;
@@ -348,7 +441,7 @@ us_status run_antidiagonal(const us_params& p, int stride, const void* Q, const 
   pa.lse2 = at<float>(ws, w.lse2);
   pa.scores = at<float>(ws, w.scores);
   pa.finalize = 1;
-  pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  pa.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.Ds)));
   pa.x3 = 0;
   pa.qraw = static_cast<const uint16_t*>(Q);
   pa.L = g.L;
@@ -469,7 +562,7 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   a.Q = static_cast<const __nv_bfloat16*>(Q);
   a.O = static_cast<__nv_bfloat16*>(O);
   a.lse = lse;
-  a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+  a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.Ds)));
   a.noncausal = (!mask && (p.flags & US_FLAG_NONCAUSAL)) ? 1 : 0;
   a.err = err;
   a.first_bad = first_bad;
@@ -640,6 +733,7 @@ us_status us_check_params(const us_params* p, const char* who, int32_t need_comp
 
 size_t us_workspace_bytes(const us_params* p) {
   if (!p || !check(*p, false).errors.empty()) return 0;
+  if (needs_pad(*p) && p->d_k <= 128) return padded_ws_bytes(*p);
   return layout(*p).total;
 }
 
@@ -651,6 +745,20 @@ us_status us_compress(const us_params* p, const void* Q, const void* K, float* Q
   if (s != US_OK) return s;
   Geo g(*p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (needs_pad(*p)) {
+    PadStage ps;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "compress", ps)) != US_OK) return s;
+    if ((s = pad_inputs(*p, ps, Q, K, nullptr, st)) != US_OK) return s;
+    float* qc = reinterpret_cast<float*>(ps.base + ps.w.qc);
+    float* kc = reinterpret_cast<float*>(ps.base + ps.w.kc);
+    if ((s = us_compress(&ps.pp, ps.base + ps.w.q, ps.base + ps.w.k, qc, kc, workspace, ps.inner_bytes, stream)) !=
+        US_OK)
+      return s;
+    if ((s = unpad_rows(qc, Qc, size_t(g.B) * g.Hc * g.Lq, g.D, ps.pp.d_k, 4, st)) != US_OK) return s;
+    if ((s = unpad_rows(kc, Kc, size_t(g.B) * g.Hc * g.Lk, g.D, ps.pp.d_k, 4, st)) != US_OK) return s;
+    if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "compress");
+    return US_OK;
+  }
   // reference layout: H/c_h planes for both Q and K (K expanded to H heads first)
   CompressArgs cq{static_cast<const uint16_t*>(Q), g.B, g.H, g.L, g.D, p->c_q, g.Hc, p->c_h, 1, Qc, nullptr,
                   p->strategy, 0, p->seed, p->head0, nullptr, nullptr, nullptr, p->dtype == US_DTYPE_F32};
@@ -666,10 +774,17 @@ us_status us_select(const us_params* p, const void* Q, const void* K, const us_s
                     void* workspace, size_t workspace_bytes, void* stream) {
   us_status s = gate(p, "select_blocks", true);
   if (s != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (needs_pad(*p)) {
+    PadStage ps;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "select_blocks", ps)) != US_OK) return s;
+    if ((s = pad_inputs(*p, ps, Q, K, nullptr, st)) != US_OK) return s;
+    ScaleDk scale(p->d_k);
+    return us_select(&ps.pp, ps.base + ps.w.q, ps.base + ps.w.k, out, workspace, ps.inner_bytes, stream);
+  }
   if ((s = need_ws(*p, workspace, workspace_bytes, "select_blocks")) != US_OK) return s;
   Geo g(*p);
   Ws w = layout(*p);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   ProxyArgs pa{};
   if ((s = run_proxy(*p, Q, K, workspace, st, &pa)) != US_OK) return s;
   uint32_t* mask = (out && out->mask_bits) ? out->mask_bits : at<uint32_t>(workspace, w.mask);
@@ -682,12 +797,17 @@ size_t us_proxy_workspace_bytes(const us_params* p, int32_t proxy, int32_t strid
   if (!p || !check(*p, false).errors.empty()) return 0;
   if (proxy == US_PROXY_ANTIDIAGONAL && stride > 0) return layout(antidiag_params(*p, stride), true).total;
   if (proxy == US_PROXY_LAST_BLOCK) return layout(antidiag_params(*p, p->S), true).total;
-  return layout(*p).total;
+  return us_workspace_bytes(p);
 }
 
 us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, const void* Q, const void* K,
                           const us_selection* out, void* workspace, size_t workspace_bytes, void* stream) {
   if (proxy == US_PROXY_UNISPARSE) return us_select(p, Q, K, out, workspace, workspace_bytes, stream);
+  if (p && needs_pad(*p) && p->d_k <= 128) {
+    set_error("select_blocks: d_k=" + std::to_string(p->d_k) +
+              " is supported by the UniSparse proxy only on the GPU path (competitor proxies: 64 or 128)");
+    return US_ERR_UNSUPPORTED;
+  }
   us_status s = gate(p, "select_blocks", false);
   if (s != US_OK) return s;
   if (proxy == US_PROXY_LAST_BLOCK) {
@@ -709,7 +829,7 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
     la.D = g.D;
     la.Q = static_cast<const uint16_t*>(Q);
     la.K = static_cast<const uint16_t*>(K);
-    la.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.D)));
+    la.scale_log2 = float(1.4426950408889634 / std::sqrt(double(g.Ds)));
     const size_t stat = size_t(g.B) * g.H * (g.L / 256) * 64;
     la.cmax = at<float>(workspace, w.part);
     la.csum = la.cmax + stat;
@@ -758,6 +878,8 @@ us_status us_select_proxy(const us_params* p, int32_t proxy, int32_t stride, con
 // ---------------------------------------------------------------- quality metrics (§8f-4)
 size_t us_mass_workspace_bytes(const us_params* p) {
   if (!p || !check(*p, false).errors.empty()) return 0;
+  if (needs_pad(*p) && p->d_k <= 128)
+    return al(layout(antidiag_params(padded_params(*p), 1), true).total) + pad_layout(*p).total;
   return layout(antidiag_params(*p, 1), true).total;
 }
 
@@ -771,6 +893,15 @@ us_status us_exact_block_mass(const us_params* p, const void* Q, const void* K, 
   if (!mass) {
     set_error("exact_block_mass: null output");
     return US_ERR_INVALID_ARGUMENT;
+  }
+  if (needs_pad(*p)) {
+    PadStage ps;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "exact_block_mass", ps,
+                       layout(antidiag_params(padded_params(*p), 1), true).total)) != US_OK)
+      return s;
+    if ((s = pad_inputs(*p, ps, Q, K, nullptr, static_cast<cudaStream_t>(stream))) != US_OK) return s;
+    ScaleDk scale(p->d_k);
+    return us_exact_block_mass(&ps.pp, ps.base + ps.w.q, ps.base + ps.w.k, mass, workspace, ps.inner_bytes, stream);
   }
   const us_params q = antidiag_params(*p, 1);
   if ((s = need_ws(q, workspace, workspace_bytes, "exact_block_mass", true)) != US_OK) return s;
@@ -943,6 +1074,20 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
   }
   Geo g(*p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (needs_pad(*p)) {
+    PadStage ps;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "block_sparse_attention", ps)) != US_OK) return s;
+    if ((s = pad_inputs(*p, ps, Q, K, V, st)) != US_OK) return s;
+    {
+      ScaleDk scale(p->d_k);
+      if ((s = us_sparse_attention(&ps.pp, ps.base + ps.w.q, ps.base + ps.w.k, ps.base + ps.w.v, mask_bits,
+                                   heads_per_plane, ps.base + ps.w.o, lse, workspace, ps.inner_bytes, stream)) != US_OK)
+        return s;
+    }
+    if ((s = unpad_rows(ps.base + ps.w.o, O, size_t(g.B) * g.H * g.L, g.D, ps.pp.d_k, 2, st)) != US_OK) return s;
+    if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "block_sparse_attention");
+    return US_OK;
+  }
   if (p->flags & US_FLAG_SYNC_CHECK) {
     if ((s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK) return s;
     Ws w = layout(*p);
@@ -979,10 +1124,23 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
   // unisparse_attn validates through select_blocks (pipeline.cpp:19-24 -> :7-8)
   us_status s = gate(p, "select_blocks", true);
   if (s != US_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (needs_pad(*p)) {
+    PadStage ps;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "unisparse_attn", ps)) != US_OK) return s;
+    if ((s = pad_inputs(*p, ps, Q, K, V, st)) != US_OK) return s;
+    {
+      ScaleDk scale(p->d_k);
+      if ((s = us_unisparse_attention(&ps.pp, ps.base + ps.w.q, ps.base + ps.w.k, ps.base + ps.w.v, ps.base + ps.w.o,
+                                      lse, sel, workspace, ps.inner_bytes, stream)) != US_OK)
+        return s;
+    }
+    Geo g(*p);
+    return unpad_rows(ps.base + ps.w.o, O, size_t(g.B) * g.H * g.L, g.D, ps.pp.d_k, 2, st);
+  }
   if ((s = need_ws(*p, workspace, workspace_bytes, "unisparse_attn")) != US_OK) return s;
   Geo g(*p);
   Ws w = layout(*p);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int call = g_prof.on() ? g_prof.next++ : -1;
   g_prof.mark(call, 0, st);
   ProxyArgs pa{};
@@ -1002,8 +1160,21 @@ us_status us_dense_attention(const us_params* p, const void* Q, const void* K, c
                              void* stream) {
   us_status s = gate(p, "dense_attention", false);
   if (s != US_OK) return s;
-  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "dense_attention")) != US_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (needs_pad(*p)) {
+    PadStage ps;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "dense_attention", ps)) != US_OK) return s;
+    if ((s = pad_inputs(*p, ps, Q, K, V, st)) != US_OK) return s;
+    {
+      ScaleDk scale(p->d_k);
+      if ((s = us_dense_attention(&ps.pp, ps.base + ps.w.q, ps.base + ps.w.k, ps.base + ps.w.v, ps.base + ps.w.o, lse,
+                                  workspace, ps.inner_bytes, stream)) != US_OK)
+        return s;
+    }
+    Geo g(*p);
+    return unpad_rows(ps.base + ps.w.o, O, size_t(g.B) * g.H * g.L, g.D, ps.pp.d_k, 2, st);
+  }
+  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "dense_attention")) != US_OK) return s;
   if ((s = run_attention(*p, Q, K, V, nullptr, 1, O, lse, st, nullptr, nullptr, workspace)) != US_OK) return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "dense_attention");
   return US_OK;

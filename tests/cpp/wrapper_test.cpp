@@ -73,7 +73,8 @@ static void cpu_tests() {
   m = expect_throw<std::invalid_argument>([&] { u::dense_attention(in); });
   CHECK(m == "dense_attention: d_k must be positive");
   // valid for the reference, outside the GPU path: domain_error, not invalid_argument
-  in.d_k = 96;
+  // (d_k <= 128 runs zero-padded; above 128 is outside the GPU path)
+  in.d_k = 160;
   cfg = u::CompressionConfig();
   m = expect_throw<std::domain_error>([&] { u::select_blocks(in, cfg); });
   CHECK(m.find("unsupported on the GPU path") != std::string::npos);

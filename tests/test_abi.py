@@ -56,10 +56,27 @@ def test_check_params_reference_messages(lib):
     p = UsParams(1, 4, 4, 1000, 64, 64, 8, 8, 1, 0, 0, 0, 0.95, 0, 0, 0)
     assert lib.us_check_params(C.byref(p), b"select_blocks", 1) == 1
     assert lib.us_last_error().decode() == "select_blocks: L=1000 not divisible by S=64"
-    p.L, p.d_k = 1024, 96
+    p.L, p.d_k = 1024, 160
     assert lib.us_check_params(C.byref(p), b"select_blocks", 1) == 2  # US_ERR_UNSUPPORTED
+    assert lib.us_last_error().decode() == "select_blocks: d_k=160 unsupported on the GPU path (at most 128)"
+    p.d_k = 96  # any d_k <= 128: zero-padded to 128 in the workspace
+    assert lib.us_check_params(C.byref(p), b"select_blocks", 1) == 0
     p.d_k = 128
     assert lib.us_check_params(C.byref(p), b"select_blocks", 1) == 0
+
+
+def test_padded_dk_workspace_bytes(lib):
+    """d_k outside {64, 128}: the workspace holds the inner call's workspace at the padded
+    width plus the zero-padded copies of Q, K, V, O and the compressed rows."""
+    from paper_2512_14082_b200.api import UsParams
+    lib.us_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+    lib.us_workspace_bytes.restype = C.c_size_t
+    p = UsParams(1, 4, 2, 1024, 32, 64, 8, 8, 1, 0, 0, 0, 0.95, 0, 0, 0)
+    ws32 = lib.us_workspace_bytes(C.byref(p))
+    p.d_k = 64
+    ws64 = lib.us_workspace_bytes(C.byref(p))
+    padded = 2 * 64 * 1024 * (4 + 2 + 2 + 4) + 4 * 64 * 128 * 4 * 2  # Q, K, V, O bf16 + Qc, Kc f32
+    assert ws32 >= ws64 + padded
 
 
 def test_cpp_wrapper_cpu():

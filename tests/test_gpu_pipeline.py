@@ -175,9 +175,10 @@ def test_validation_errors_match_reference():
     q = torch.zeros((1, 4, 1024, 128), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError, match="not divisible by c_q=24"):
         us().select_blocks(q, q, us().CompressionConfig(c_q=24))
-    q96 = torch.zeros((1, 4, 1024, 96), dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(us().UnsupportedError):
-        us().select_blocks(q96, q96, us().CompressionConfig())
+    # d_k <= 128 runs zero-padded (tests/test_gpu_dk.py); above 128 is outside the GPU path
+    q160 = torch.zeros((1, 4, 1024, 160), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(us().UnsupportedError, match="d_k=160 unsupported on the GPU path"):
+        us().select_blocks(q160, q160, us().CompressionConfig())
 
 
 def test_run_host_pipelined_equals_device_path():
