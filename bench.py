@@ -631,6 +631,12 @@ def main():
                 "peak": tf_sust, "unit": "TFLOP/s", "frac": achieved / tf_sust,
                 "algorithmic": "selected_blocks * 4 * S^2 * d (metrics.cpp:83-85)",
                 "issued_tflops": issued_attn / (stage_ms["attention"] * 1e-3) / 1e12 if issued_attn else None}
+        if issued_attn:
+            # M = 128 UMMA tiles hold two 64-row query groups and run S / P.V for the union of
+            # their selections; an M = 64 MMA costs the cycles of M = 128, so the useful fraction
+            # is capped at rows_useful_fraction x the issued fraction (DESIGN.md §3 a6)
+            roof["issued_frac"] = roof["issued_tflops"] / tf_sust
+            roof["rows_useful_fraction"] = tile_eff["rows_useful_fraction"]
     else:
         Lq = L // 8
         fl = 2 * Lq * Lq * len(heads) * len(shard.batch) * d  # compressed_qk (metrics.cpp:60), post-softmax full square
