@@ -228,6 +228,11 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_sempty[grp]);
 
+#ifdef US_PROXY_SKELETON
+      // calibration: MMA-pipeline rate with a math-free epilogue (results are garbage)
+      if (v[0] == 0x7fffffffu && v[127] == 0x7fffffffu) a.tmax[0] = 1.f;
+      continue;
+#endif
       const int nvalid = min(max(live - t * kKeys, 0), kKeys);
       float x[kKeys];
       float m8[8];
