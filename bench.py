@@ -688,7 +688,8 @@ def main():
     out = dict(base, value=ms, ms_per_step=ms, config=config, clocks=clk,
                e2e={"value": e2e_ms, "unit": "ms/layer", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": f"Engine.run_host(wait=False): pinned host Q/K/V -> H2D -> hot path -> D2H O, "
-                            f"{args.e2e_chunks} KV-head chunks on 3 streams, consecutive steps overlapped per chunk",
+                            f"{args.e2e_chunks} KV-head chunks on 4 streams (copy-in, 2 compute with 2 chunk workspaces, copy-out), "
+                            f"consecutive steps overlapped per chunk",
                     "serial_ms": e2e_serial_ms,
                     "output_equals_device_path": e2e_exact},
                gpu_launches=launches_per_step * args.steps,

@@ -541,9 +541,12 @@ class Engine:
 
     def _run_host(self, Qh, Kh, Vh, Oh, chunks: int = 4, wait: bool = True):
         """unisparse_attn from (pinned) host buffers: H2D of Q/K/V, the hot path,
-        D2H of O, pipelined over KV-head chunks on three CUDA streams (copy-in,
-        compute, copy-out) so the PCIe transfers overlap the kernels. Enqueues
-        only; returns the event recorded after the last D2H on the copy-out stream.
+        D2H of O, pipelined over KV-head chunks on CUDA streams (copy-in, two
+        compute streams, copy-out) so the PCIe transfers overlap the kernels and
+        consecutive chunks' kernels overlap each other's tails (chunk c computes on
+        stream c % 2 with its own chunk-sized workspace carved from the engine's).
+        Enqueues only; returns the event recorded after the last D2H on the copy-out
+        stream.
 
         wait=True: the current stream waits for that event (the call is ordered
         like any other stream op). wait=False: it does not, so back-to-back calls
@@ -554,8 +557,8 @@ class Engine:
         plan = self._chunk_plan(chunks) if chunks > 1 else None
         cur = torch.cuda.current_stream()
         if not hasattr(self, "_streams"):
-            self._streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
-        s_in, s_comp, s_out = self._streams
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+        s_in, s_comp, s_out, s_comp2 = self._streams
         start = torch.cuda.Event()
         start.record(cur)
         for s_ in self._streams:
@@ -580,7 +583,16 @@ class Engine:
             self._chunk_events = (done, [])
             return done
         G = self.p.H // self.p.H_kv
-        ws = _ptr(self.ws)
+        # two chunk-sized workspaces (one per compute stream) inside the layer's workspace
+        wsz = max(int(lib().us_workspace_bytes(C.byref(cp))) for cp, _, _, _ in plan)
+        wsz = (wsz + 255) // 256 * 256
+        if 2 * wsz > self.ws.numel():
+            if getattr(self, "_ws2", None) is None or self._ws2.numel() < 2 * wsz:
+                self._ws2 = torch.empty(2 * wsz, dtype=torch.uint8, device=self.ws.device)
+            wbase = self._ws2
+        else:
+            wbase = self.ws
+        comp = (s_comp, s_comp2)
         events = []
         for c, (cp, (q0, q1), (k0, k1), sel) in enumerate(plan):
             e_in, e_comp, e_out = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
@@ -591,14 +603,15 @@ class Engine:
                 self.K[:, k0:k1].copy_(Kh[:, k0:k1], non_blocking=True)
                 self.V[:, k0:k1].copy_(Vh[:, k0:k1], non_blocking=True)
                 e_in.record(s_in)
-            s_comp.wait_event(e_in)
+            sc = comp[c % 2]
+            sc.wait_event(e_in)
             if prev is not None:
-                s_comp.wait_event(prev[1][c][1])  # ... and copied O chunk c out
+                sc.wait_event(prev[1][c][1])  # ... and copied O chunk c out
             _raise(lib().us_unisparse_attention(
                 C.byref(cp), _ptr(self.Q[:, q0:q1]), _ptr(self.K[:, k0:k1]), _ptr(self.V[:, k0:k1]),
-                _ptr(self.O[:, q0:q1]), _ptr(self.lse[:, q0:q1]), C.byref(sel), ws, self.ws.numel(),
-                C.c_void_p(s_comp.cuda_stream)))
-            e_comp.record(s_comp)
+                _ptr(self.O[:, q0:q1]), _ptr(self.lse[:, q0:q1]), C.byref(sel),
+                C.c_void_p(wbase.data_ptr() + (c % 2) * wsz), wsz, C.c_void_p(sc.cuda_stream)))
+            e_comp.record(sc)
             s_out.wait_event(e_comp)
             with torch.cuda.stream(s_out):
                 Oh[:, q0:q1].copy_(self.O[:, q0:q1], non_blocking=True)
