@@ -111,16 +111,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ float xl[2][128][2];  // row-sum exchange (epilogue)
   // union positions whose K / V load the producers have issued (published for the issuers)
   __shared__ int k_issued, v_issued;
-#ifdef US_WATCHDOG_PRINT
-  __shared__ volatile int dbg_iss[2][5];   // k, ns, pos0, pos1, state
-  __shared__ volatile int dbg_sm[2][8][2]; // kk, state
-  __shared__ volatile int dbg_vprod;
-#define DBG_ISS(f, v) dbg_iss[x][f] = (v)
-#define DBG_SM(st) dbg_sm[x][(warp - 4) & 7][1] = (st)
-#else
-#define DBG_ISS(f, v)
-#define DBG_SM(st)
-#endif
 
   const int warp = threadIdx.x >> 5;
 #if US_TP_TRACE
@@ -136,10 +126,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_q[x], 1);
       mbar_init(&bar_sfull[x][0], 1);
       mbar_init(&bar_sfull[x][1], 1);
-#ifdef US_WATCHDOG_PRINT
-      for (int i = 0; i < 10; ++i) (&dbg_iss[0][0])[i] = -1;
-      for (int i = 0; i < 32; ++i) (&dbg_sm[0][0][0])[i] = -1;
-#endif
       // one P barrier per buffer: a softmax warp may finish step k + 1 before another
       // finishes step k, so the arrivals of consecutive steps must not share a barrier
       mbar_init(&bar_pfull[x][0], 8);
@@ -159,12 +145,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     v_issued = 0;
     fence_barrier_init();
   }
-#ifdef US_WATCHDOG_PRINT
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    printf("bars: q %x kfull %x kempty %x vfull %x vempty %x sfull %x pfull %x pvdone %x ofull %x\n", smem_u32(bar_q),
-           smem_u32(bar_kfull), smem_u32(bar_kempty), smem_u32(bar_vfull), smem_u32(bar_vempty), smem_u32(bar_sfull),
-           smem_u32(bar_pfull), smem_u32(bar_pvdone), smem_u32(bar_ofull));
-#endif
   if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
   if (warp == 2) attn::build_lists(a, gr, jmax, a.pairing != 0, ls, nullptr);
   tc_fence_before();
@@ -197,34 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < T; ++t) {
         const int j = int(ls.steps[t] & 0xFFFu);
         const int s = t % kSK;
-#ifdef US_WATCHDOG_PRINT
-        if (t >= kSK) {
-          const long long t0 = clock64();
-          while (!mbar_try_wait(&bar_kempty[s], ((t / kSK) + 1) & 1))
-            if (clock64() - t0 > 2000000000ll) {
-              printf("K producer stuck: block %d t %d T %d n_own %d %d | iss A k %d ns %d pos %d %d st %d | iss B k %d ns %d pos %d %d st %d\n",
-                     int(blockIdx.x), t, T, ls.n_own[0], ls.n_own[1], dbg_iss[0][0], dbg_iss[0][1], dbg_iss[0][2], dbg_iss[0][3], dbg_iss[0][4],
-                     dbg_iss[1][0], dbg_iss[1][1], dbg_iss[1][2], dbg_iss[1][3], dbg_iss[1][4]);
-              for (int xx = 0; xx < 2; ++xx)
-                printf("  block %d tile %d softmax kk/state: %d/%d %d/%d %d/%d %d/%d %d/%d %d/%d %d/%d %d/%d\n", int(blockIdx.x), xx,
-                       dbg_sm[xx][0][0], dbg_sm[xx][0][1], dbg_sm[xx][1][0], dbg_sm[xx][1][1], dbg_sm[xx][2][0], dbg_sm[xx][2][1], dbg_sm[xx][3][0], dbg_sm[xx][3][1],
-                       dbg_sm[xx][4][0], dbg_sm[xx][4][1], dbg_sm[xx][5][0], dbg_sm[xx][5][1], dbg_sm[xx][6][0], dbg_sm[xx][6][1], dbg_sm[xx][7][0], dbg_sm[xx][7][1]);
-              {
-                char buf[160]; int n = 0;
-                for (int u = 0; u < T && n < 150; ++u) n += 0;
-                (void)buf;
-              }
-              for (int u = 0; u < T; u += 8)
-                printf("  block %d steps[%d..]: %x %x %x %x %x %x %x %x\n", int(blockIdx.x), u, ls.steps[u], u + 1 < T ? ls.steps[u + 1] : 0,
-                       u + 2 < T ? ls.steps[u + 2] : 0, u + 3 < T ? ls.steps[u + 3] : 0, u + 4 < T ? ls.steps[u + 4] : 0,
-                       u + 5 < T ? ls.steps[u + 5] : 0, u + 6 < T ? ls.steps[u + 6] : 0, u + 7 < T ? ls.steps[u + 7] : 0);
-              printf("  block %d vprod t %d\n", int(blockIdx.x), dbg_vprod);
-              __trap();
-            }
-        }
-#else
         if (t >= kSK) mbar_wait(&bar_kempty[s], ((t / kSK) + 1) & 1);
-#endif
         mbar_arrive_expect_tx(&bar_kfull[s], SL::kTileBytes);
         // one 3-D TMA per tile: 64 rows x all d-chunks, landing as [chunk][row][128 B]
         tma_load_3d_hint(smem + SL::kKRing + s * SL::kTileBytes, &tmK, &bar_kfull[s], 0, kvrow0 + j * kBS, 0,
@@ -247,9 +200,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < T; ++t) {
         const int j = int(ls.steps[t] & 0xFFFu);
         const int s = t % kSV;
-#ifdef US_WATCHDOG_PRINT
-        dbg_vprod = t;
-#endif
         if (t >= kSV) mbar_wait(&bar_vempty[s], ((t / kSV) + 1) & 1);
         mbar_arrive_expect_tx(&bar_vfull[s], SL::kTileBytes);
         tma_load_3d_hint(smem + SL::kVRing + s * SL::kTileBytes, &tmV, &bar_vfull[s], 0, kvrow0 + j * kBS, 0,
@@ -282,10 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[p % nst], (p / nst) & 1);
     };
     auto issue_s = [&](int tt, int kk) {  // S(kk) from union position tt into buffer kk & 1
-      DBG_ISS(4, 1);
-      DBG_ISS(1, kk);
       wait_loaded(bar_kfull, &k_issued, tt, kSK);
-      DBG_ISS(4, 2);
       TPTRACE((threadIdx.x & 31) == 0, x, kk, 12);
       tc_fence_after();
       if (elect_one()) {
@@ -324,17 +271,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     issue_ready(-1);
     for (int k = 0; k < n_own; ++k) {
-      DBG_ISS(0, k);
-      DBG_ISS(2, pos[0]);
-      DBG_ISS(3, pos[1]);
-      DBG_ISS(4, 3);
       mbar_wait(&bar_pfull[x][k & 1], (k >> 1) & 1);  // P(k) of all 128 rows is in TMEM
-      DBG_ISS(4, 4);
       TPTRACE((threadIdx.x & 31) == 0, x, k, 6);
       tc_fence_after();
       const int t = pos[0];
       wait_loaded(bar_vfull, &v_issued, t, kSV);
-      DBG_ISS(4, 5);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sV = smem_u32(smem + SL::kVRing + (t % kSV) * SL::kTileBytes);
@@ -380,11 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int j = int(e & 0xFFFu);
       const bool sel = (e >> (12 + slot)) & 1u;  // warp-uniform (32 rows of one group)
       const uint32_t sb = tb + (kk & 1) * 64 + c_half;  // this half's S / P columns
-#ifdef US_WATCHDOG_PRINT
-      if (lane == 0) { dbg_sm[x][(warp - 4) & 7][0] = kk; DBG_SM(1); }
-#endif
       mbar_wait(&bar_sfull[x][kk & 1], (kk >> 1) & 1);
-      if (lane == 0) DBG_SM(2);
       TPTRACE(row == 0, x, kk, hf ? 8 : 1);
       tc_fence_after();
       uint32_t packed[16];
@@ -411,9 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         float (*xb)[2] = xch[kk & 1][x];
         xb[row][hf] = hm;
-        if (lane == 0) DBG_SM(3);
         named_bar_sync(bar_id, 64);
-        if (lane == 0) DBG_SM(4);
         const float mx = fmaxf(hm, xb[row][hf ^ 1]) * sl2;
         TPTRACE(row == 0, x, kk, hf ? 9 : 3);
         // lazy rescale: both halves of a row take the same decision (same mx)
@@ -422,9 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (__any_sync(0xffffffffu, need_o)) {
           // O must hold every key before this step: wait for P.V(kk - 1). Warp-collective
           // TMEM ld/st; rows that did not move use f = 1.
-          if (lane == 0) DBG_SM(5);
           mbar_wait(&bar_pvdone[x], (kk - 1) & 1);
-          if (lane == 0) DBG_SM(6);
           tc_fence_after();
           const float f = need_o ? ex2_approx(m_used - mx) : 1.f;
 #pragma unroll 1
@@ -483,7 +416,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       TPTRACE(lane == 0 && q == 0, x, kk, hf ? 10 : 5);
       TPTRACE(lane == 0 && q == 3 && hf == 0, x, kk, 11);
     }
-    if (lane == 0) DBG_SM(9);
     // ---- epilogue: row sum of both halves, this half of the O columns
     xl[x][row][hf] = l;
     named_bar_sync(bar_id, 64);
