@@ -75,6 +75,15 @@ __device__ int g_attn_trace_cta;
   } while (0)
 #endif
 
+// Calibration knob: 1 = skipped union positions are released by the TMA producer on behalf
+// of the tile that skips them instead of by that tile's issuer when its own walk reaches
+// them (a lagging tile then never holds ring stages it does not use). Measured neutral at
+// C3 (profiles/r02c/README.md): the sparse step is bound by the selected group's softmax
+// chain, not by the ring. Default 0 (the issuer walk).
+#ifndef US_ATTN_PRODUCER_RELEASE
+#define US_ATTN_PRODUCER_RELEASE 0
+#endif
+
 namespace us {
 namespace {
 
@@ -156,6 +165,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       bar_pvdone[2], bar_ofull[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ attn::Lists ls;
+  __shared__ int kv_issued;  // union positions whose K/V load the producer has issued
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if US_ATTN_TRACE
@@ -180,6 +190,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
     }
     mbar_init(&bar_ofull[0], 1);
     mbar_init(&bar_ofull[1], 1);
+    kv_issued = 0;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&tmem_base_sh, NT * 256);
@@ -207,6 +218,13 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
         // one 3-D TMA per tile: 64 rows x all d-chunks, landing as [chunk][row][128 B]
         tma_load_3d_hint(sk, &tmK, &bar_kvfull[s], 0, kvrow0 + j * kBS, 0, pol_kv);
         tma_load_3d_hint(sv, &tmV, &bar_kvfull[s], 0, kvrow0 + j * kBS, 0, pol_kv);
+#if US_ATTN_PRODUCER_RELEASE
+        // a tile that skips this position releases it right away (the producer arrives
+        // for it); the issuers learn which loads exist from kv_issued
+        for (int x = 0; x < NT; ++x)
+          if (((ls.steps[t] >> (12 + 2 * x)) & 3u) == 0u) mbar_arrive(&bar_kvempty[s]);
+        *reinterpret_cast<volatile int*>(&kv_issued) = t + 1;
+#endif
       }
     }
     __syncwarp();
@@ -223,12 +241,26 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
     // Release union positions [from, to) this tile skips. Waiting for each tile to
     // land keeps this warp's kv_empty arrivals in phase order (one per stage phase).
     auto release = [&](int from, int to) {
+#if US_ATTN_PRODUCER_RELEASE
+      (void)from;
+      (void)to;
+#else
       for (int tt = from; tt < to; ++tt) {
         mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
         if (lane == 0) mbar_arrive(&bar_kvempty[tt % kST]);
       }
+#endif
     };
     auto issue_s = [&](int tt, int kk) {
+      if (lane == 0) TRACE(x, kk, 7);  // issuer ready to issue S(kk)
+#if US_ATTN_PRODUCER_RELEASE
+      // Parity waits are only meaningful within one phase of a barrier, and this tile's
+      // own positions can be far apart while the stage advances on positions it skips:
+      // wait on kvfull(tt) only once the producer has ISSUED load tt, which implies load
+      // tt - kST landed (its release needed it) — the barrier is at most one phase behind,
+      // and it cannot be ahead (this tile still holds tt).
+      while (*reinterpret_cast<const volatile int*>(&kv_issued) <= tt) __nanosleep(20);
+#endif
       mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
       if (lane == 0) TRACE(x, kk, 8);  // K/V of the step has landed
       tc_fence_after();
@@ -256,6 +288,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       const int tn = own_at(k + 1);
       const bool early = tn < T && tn - t < kST;
       mbar_wait(&bar_sfree[x], k & 1);  // the softmax has loaded S(k): S columns are free
+      if (lane == 0) TRACEV(x, k, 14, clock64());  // S(k) freed
       if (early) {
         release(t + 1, tn);
         issue_s(tn, k + 1);

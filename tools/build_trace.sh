@@ -9,5 +9,5 @@ mkdir -p $B
 F="-gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -ccbin /usr/bin/g++ -Ipaper_2512_14082_b200/csrc -DUS_CALIBRATION"
 O=paper_2512_14082_b200/_build/calib  # calibration-build objects (-DUS_CALIBRATION)
 nvcc $F -DUS_ATTN_TRACE=1 "$@" -c $SRC -o $B/attention.o
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $B/libunisparse_trace.so $O/api.o $O/compress.o $O/proxy.o $O/select.o $B/attention.o $O/attention2.o $O/attention_kt.o $O/lastblock.o $O/io.o $O/metrics.o $O/selftest.o -lrt
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $B/libunisparse_trace.so $(ls $O/*.o | grep -v "/attention.o") $B/attention.o -lrt
 echo $B/libunisparse_trace.so
