@@ -110,3 +110,29 @@ def test_padded_dk_needs_workspace():
                                       0, None)
     assert st == api.US_ERR_WORKSPACE
     assert "zero-padded to 64" in api.lib().us_last_error().decode()
+
+
+@pytest.mark.parametrize("d,S", [(32, 64), (32, 128), (96, 128)])
+def test_padded_dk_f32_inputs_and_block_size(d, S):
+    """d_k padding composed with the other staging paths: the reference's own un-rounded
+    f32 storage (us_params.dtype = F32) and the battery's block size S = 128 — masks
+    bit-exact vs the oracle on the f32 inputs, outputs within the bf16 bound."""
+    L, H, H_kv, P = 2048, 4, 2, 0.95
+    Q, K, V, _ = O.gen_workload(O.WL_PLANTED, L, H, d, S, 77 + d + S, H_kv=H_kv, gain=8.0)  # f32, not rounded
+    c = O.cfg(H, L, d, S, H_kv=H_kv, P=P)
+    Or, lser, ref_mask, _ = O.unisparse_attn(c, Q, K, V)
+    f32 = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).unsqueeze(0).cuda().contiguous()
+    cfg = us().CompressionConfig(P=P)
+    res = us().unisparse_attn(f32(Q), f32(K), f32(V), cfg, S=S)
+    torch.cuda.synchronize()
+    gmask = res.report.mask.dense_mask()[0].cpu().numpy()
+    assert (gmask == ref_mask).all(), int((gmask != ref_mask).sum())
+    Og = res.O[0].float().cpu().numpy()
+    assert Og.shape[-1] == d
+    # attention runs on bf16 copies of the f32 inputs (DESIGN §1): compared with the fp64
+    # oracle on those same bf16 values over the (bit-exact) mask. Against the f32 inputs
+    # themselves the bf16 rounding alone moves O by ~1 % at d = 32 with gain-8 logits.
+    Ob, lseb = O.block_sparse_attention(O.bf16_round(Q), O.bf16_round(K), O.bf16_round(V), ref_mask, S)
+    assert np.abs(Og - Ob).max() <= 1e-2 * np.abs(Ob).max() + 1e-4
+    assert np.linalg.norm(Og - Ob) / np.linalg.norm(Ob) <= 1e-2
+    assert np.abs(res.lse[0].cpu().numpy() - lseb).max() <= 1e-3 * max(1.0, np.abs(lseb).max())
