@@ -182,15 +182,18 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, int N, int 
   long long t0 = clock64();
   if (warp == 0) {
     if (elect_one()) {
-      const uint32_t idesc = idesc_f16(128, N, 1, false, false);
+      // a_tmem bit 0: A from TMEM; bit 1: M = 64; bit 2: alternate the accumulator (and TMEM A)
+      // between lane offsets 0 and 16 per MMA (two M = 64 products sharing columns)
+      const uint32_t idesc = idesc_f16((a_tmem & 2) ? 64 : 128, N, 1, false, false);
       const uint32_t sb = smem_u32(smem);
       for (int it = 0; it < iters; ++it) {
         for (int k = 0; k < per_group; ++k) {
           const uint64_t bd = sdesc_sw128(sb + 32768 + (k & 3) * 32, 16, 1024);
-          if (a_tmem)
-            umma_f16_ts(tmem, tmem + 256 + (k & 7) * 8, bd, idesc, k > 0);
+          const uint32_t lo = ((a_tmem & 4) && (k & 1)) ? (16u << 16) : 0u;
+          if (a_tmem & 1)
+            umma_f16_ts(tmem + lo, tmem + lo + 256 + (k & 7) * 8, bd, idesc, k > 1);
           else
-            umma_f16_ss(tmem, sdesc_sw128(sb + (k & 3) * 32, 16, 1024), bd, idesc, k > 0);
+            umma_f16_ss(tmem + lo, sdesc_sw128(sb + (k & 3) * 32, 16, 1024), bd, idesc, k > 1);
         }
       }
       umma_commit(&bar);
@@ -536,5 +539,125 @@ extern "C" us_status us_selftest_softmax_probe(int iters, int mode, int ctas, in
   using namespace us;
   softmax_probe_kernel<<<ctas, threads, 0, static_cast<cudaStream_t>(stream)>>>(iters, mode, sink, cycles_out);
   US_LAUNCH_CHECK("us_selftest_softmax_probe");
+  return US_OK;
+}
+
+// ---------------------------------------------------------------- M = 64 accumulator layout probe
+// One M = 64, N = 64, K = 128 kind::f16 MMA (A rows 0-63 and B both K-major SW128 in smem,
+// written by threads) with the accumulator address at TMEM lane offset `lane_off`; TMEM
+// columns [0, 64) of all 128 lanes are first filled with a sentinel and read back after, so
+// the host sees which lanes the 64 result rows land in (D_out [128 lanes][64 cols] f32).
+namespace us {
+namespace {
+// ts = 1: A from TMEM instead — A2 [128][128] bf16 rows 64 r + ... : rows 0-63 of A at lanes
+// (16 q + r) of quarter q (offset 0), rows 64-127 at lanes 16 + (16 q + r) (offset 16), in
+// TMEM columns [64, 128); two MMAs: D at offset 0 with A offset 0, D at offset 16 (columns
+// [0, 64)) with A offset 16 — then D_out holds both results.
+__global__ void __launch_bounds__(128, 1)
+    m64_probe_kernel(const uint16_t* __restrict__ A, const uint16_t* __restrict__ B, int lane_off, float* D_out,
+                     int ts) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;               // [kc][64 rows][128 B]
+  uint8_t* sB = smem + 64 * 128 * 2;  // [kc][64 rows][128 B]
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_mma, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base_sh, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  {
+    uint32_t v[16];
+    for (int t = 0; t < 16; ++t) v[t] = __float_as_uint(12345.0f);
+    for (int c0 = 0; c0 < 64; c0 += 16) tmem_st16(tmem + lane_base + c0, v);
+    tmem_st_wait();
+  }
+  if (threadIdx.x < 64) {
+    const int r = threadIdx.x;
+    for (int kc = 0; kc < 2; ++kc)
+      for (int ch = 0; ch < 8; ++ch) {
+        *reinterpret_cast<uint4*>(sA + kc * 64 * 128 + sw128_offset(r, ch)) =
+            *reinterpret_cast<const uint4*>(A + r * 128 + kc * 64 + ch * 8);
+        *reinterpret_cast<uint4*>(sB + kc * 64 * 128 + sw128_offset(r, ch)) =
+            *reinterpret_cast<const uint4*>(B + r * 128 + kc * 64 + ch * 8);
+      }
+  }
+  if (ts == 1 || ts >= 2) {
+    // lane 32 q + i holds A row (i < 16 ? 16 q + i : 64 + 16 q + (i - 16)); 2 bf16 per column
+    const int i = lane;
+    const int arow = i < 16 ? 16 * warp + i : 64 + 16 * warp + (i - 16);
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      uint32_t v[16];
+      for (int t = 0; t < 16; ++t)
+        v[t] = uint32_t(A[arow * 128 + 2 * (c0 + t)]) | (uint32_t(A[arow * 128 + 2 * (c0 + t) + 1]) << 16);
+      tmem_st16(tmem + lane_base + 64 + c0, v);
+    }
+    tmem_st_wait();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t idesc = idesc_f16(64, 64, 1, false, false);
+      if (ts == 0) {
+        for (int k = 0; k < 8; ++k) {
+          const int kc = k / 4, ks = k % 4;
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + kc * 64 * 128 + ks * 32), 16, 1024);
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + kc * 64 * 128 + ks * 32), 16, 1024);
+          umma_f16_ss(tmem + (uint32_t(lane_off) << 16), ad, bd, idesc, k > 0);
+        }
+      } else {
+        for (int off = 0; off < 32; off += 16)
+          for (int k = 0; k < 8; ++k) {
+            const int kc = k / 4, ks = k % 4;
+            const uint64_t bd = sdesc_sw128(smem_u32(sB + kc * 64 * 128 + ks * 32), 16, 1024);
+            umma_f16_ts(tmem + (uint32_t(off) << 16), tmem + (uint32_t(off) << 16) + 64 + k * 8, bd, idesc, k > 0);
+          }
+      }
+      umma_commit(&bar_mma);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar_mma, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  if (ts >= 2) {
+    // 16x32bx2 read of the accumulator at lane offset (ts - 2) * 16 of each quarter:
+    // D_out[warp][lane][32] = what thread `lane` of warp `warp` receives
+    uint32_t v[32];
+    tmem_ld_16x32bx2_x32<32>(tmem + lane_base + (uint32_t((ts - 2) * 16) << 16), v);
+    tmem_ld_wait();
+    for (int t = 0; t < 32; ++t) D_out[row * 64 + t] = __uint_as_float(v[t]);
+  } else {
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tmem + lane_base + c0, v);
+      tmem_ld_wait();
+      for (int t = 0; t < 16; ++t) D_out[row * 64 + c0 + t] = __uint_as_float(v[t]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 128);
+}
+}  // namespace
+}  // namespace us
+
+extern "C" us_status us_selftest_m64_layout(const void* A, const void* B, int lane_off, int ts, float* D_out,
+                                           void* stream) {
+  using namespace us;
+  const size_t smem = 32 * 1024 + 1024;
+  m64_probe_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(A), static_cast<const uint16_t*>(B), lane_off, D_out, ts);
+  US_LAUNCH_CHECK("us_selftest_m64_layout");
   return US_OK;
 }
