@@ -21,7 +21,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "libunisparse_b200.so")
-SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "lastblock.cu", "io.cu", "metrics.cu"]
+SOURCES = ["api.cu", "compress.cu", "proxy.cu", "select.cu", "attention.cu", "attention64.cu", "lastblock.cu", "io.cu", "metrics.cu"]
 CALIB_SOURCES = SOURCES + ["attention2.cu", "attention_kt.cu", "attention_tp.cu", "selftest.cu"]
 CALIB_LIB = os.path.join(OUT_DIR, "libunisparse_b200_calib.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")

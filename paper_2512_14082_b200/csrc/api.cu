@@ -171,7 +171,7 @@ struct Geo {
 
 struct Ws {
   size_t err, first_bad, fb_count, absmax_q, absmax_k, exp_q, exp_k, fb_rows, qc, kc, qh, ql, kh,
-      kl, lse2, part, tmax, scores, mask, conv, mask64, total;
+      kl, lse2, part, tmax, scores, mask, conv, mask64, items, total;
   size_t header_bytes;  // [0, header_bytes) is cleared before each selection
 };
 
@@ -221,6 +221,8 @@ Ws layout(const us_params& p, bool scores_region = false) {
   // S > 64: the 64-granular copy of the block mask the attention kernels walk (one plane per head)
   const size_t n64 = size_t(g.L) / kGpuBlock;
   w.mask64 = g.S != kGpuBlock ? take(4 * size_t(g.B) * g.H * n64 * ((n64 + 31) / 32)) : 0;
+  // attention64.cu work-item table (groups sorted by selected-block count)
+  w.items = take(4 * size_t(attention64_item_entries(g.B, g.H, g.H_kv, int(n64))) + 16);  // + the sel_pairs counter
   w.total = o;
   return w;
 }
@@ -505,17 +507,18 @@ us_status run_select_fused(const us_params& p, const ProxyArgs& pa, uint32_t* ma
 }
 
 // Attention kernel selection (calibration knob, US_ATTN_IMPL): 0 = automatic
-// (default: the key-major attention_kt.cu for block-sparse masks at d_k = 128,
-// attention.cu for dense / d_k = 64), 1 = attention.cu (two M=128 query tiles
-// per CTA, 64-key steps), 2 = attention2.cu, 3 = attention.cu with one tile per
-// CTA, 4 = attention_kt.cu whenever d_k = 128 (dense included), 5 = attention_tp.cu
-// (decoupled softmax: P in TMEM, two logit buffers per tile). 2-5: calibration build only.
+// (default: masks with the item-table workspace launch both attention64.cu and
+// attention.cu, the device-side density gate attn::m64_wins running one of them; dense
+// and workspace-less calls run attention.cu), 1 = attention.cu (two M=128 query tiles
+// per CTA, 64-key steps), 2 = attention2.cu, 3 = attention.cu with one tile per CTA,
+// 4 = attention_kt.cu whenever d_k = 128, 5 = attention_tp.cu (decoupled softmax),
+// 6 = attention64.cu for every mask (M = 64 chains). 2-5: calibration build only.
 std::atomic<int> g_attn_impl{-1};
 int attention_impl() {
   int v = g_attn_impl.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = std::getenv("US_ATTN_IMPL");
-    v = (e && std::atoi(e) >= 1 && std::atoi(e) <= 5) ? std::atoi(e) : 0;
+    v = (e && std::atoi(e) >= 1 && std::atoi(e) <= 6) ? std::atoi(e) : 0;
     g_attn_impl.store(v, std::memory_order_relaxed);
   }
   return v;
@@ -536,7 +539,7 @@ int attention_pairing() {
 // The attention kernels: bf16 Q/K/V, 64-granular masks (p.S == 64, p.dtype == bf16).
 us_status run_attention_core(const us_params& p, const void* Q, const void* K, const void* V,
                              const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st, uint32_t* err,
-                             int32_t* first_bad) {
+                             int32_t* first_bad, int32_t* items) {
   Geo g(p);
   us_status s;
   CUtensorMap tQ, tK, tV;
@@ -577,19 +580,34 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   if (impl == 2 && !a.noncausal) return launch_attention2(a, tK, tV, st);
   a.one_tile = impl == 3 ? 1 : 0;
   if (impl == 5) return launch_attention_tp(a, tQ, tK3, tV3, st);
-#else
-  (void)impl;
 #endif
+  if (impl == 6 && mask) {  // forced
+    a.items = items;
+    return launch_attention64(a, tK3, tV3, st);
+  }
+  if (impl == 0 && mask && items) {
+    // automatic: the density is known on the device only; attention64's pre-pass counts the
+    // selected pairs and each kernel's CTAs exit unless attn::m64_wins picks that kernel
+    a.items = items;
+    a.sel_pairs = reinterpret_cast<unsigned long long*>(
+        items + attention64_item_entries(g.B, g.H, g.H_kv, g.N));
+    if ((s = launch_attention64(a, tK3, tV3, st)) != US_OK) return s;
+    a.items = nullptr;
+  }
   return launch_attention(a, tQ, tK3, tV3, st);
 }
 
+// ws_ok: the caller's workspace is at least layout(p).total bytes (the attention64 item
+// table lives there; without it that kernel walks the fixed decode order).
 us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
                         const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st,
-                        uint32_t* err = nullptr, int32_t* first_bad = nullptr, void* ws = nullptr) {
+                        uint32_t* err = nullptr, int32_t* first_bad = nullptr, void* ws = nullptr,
+                        bool ws_ok = false) {
   Geo g(p);
   us_params q = p;
+  int32_t* items = (ws && ws_ok) ? at<int32_t>(ws, layout(p).items) : nullptr;
   if (p.S == kGpuBlock && p.dtype == US_DTYPE_BF16)
-    return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad);
+    return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad, items);
   if (!ws && (p.dtype == US_DTYPE_F32 || (mask && p.S != kGpuBlock))) {
     set_error("attention: f32 inputs / S != 64 need the workspace (us_workspace_bytes)");
     return US_ERR_WORKSPACE;
@@ -622,7 +640,7 @@ us_status run_attention(const us_params& p, const void* Q, const void* K, const 
     K = kb;
     V = vb;
   }
-  return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad);
+  return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad, items);
 }
 
 
@@ -703,15 +721,16 @@ int us_validate(const us_params* p, char* msg, size_t cap) {
 
 us_status us_set_attention_impl(int32_t impl) {
 #ifndef US_CALIBRATION
-  if (impl >= 2) {
+  if (impl >= 2 && impl <= 5) {
     set_error("us_set_attention_impl: implementations 2-5 are calibration variants, present only in "
               "libunisparse_b200_calib.so");
     return US_ERR_UNSUPPORTED;
   }
 #endif
-  if (impl < 0 || impl > 5) {
+  if (impl < 0 || impl > 6) {
     set_error("us_set_attention_impl: impl must be 0 (automatic), 1 (two query tiles per CTA), 2 (128-key steps), "
-              "3 (one tile per CTA), 4 (key-major) or 5 (decoupled softmax, P in TMEM)");
+              "3 (one tile per CTA), 4 (key-major), 5 (decoupled softmax, P in TMEM) or 6 (one M = 64 chain per "
+              "query group)");
     return US_ERR_INVALID_ARGUMENT;
   }
   g_attn_impl.store(impl, std::memory_order_relaxed);
@@ -1112,7 +1131,8 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
     first_bad = at<int32_t>(workspace, w.first_bad);
     US_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7F, 4, st), "workspace clear");
   }
-  if ((s = run_attention(*p, Q, K, V, mask_bits, heads_per_plane, O, lse, st, err, first_bad, workspace)) != US_OK)
+  if ((s = run_attention(*p, Q, K, V, mask_bits, heads_per_plane, O, lse, st, err, first_bad, workspace,
+                         workspace && workspace_bytes >= layout(*p).total)) != US_OK)
     return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "block_sparse_attention");
   return US_OK;
@@ -1149,7 +1169,8 @@ us_status us_unisparse_attention(const us_params* p, const void* Q, const void* 
   uint32_t* mask = (sel && sel->mask_bits) ? sel->mask_bits : at<uint32_t>(workspace, w.mask);
   if ((s = run_select_fused(*p, pa, mask, sel, workspace, st)) != US_OK) return s;
   g_prof.mark(call, 3, st);
-  if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st, nullptr, nullptr, workspace)) != US_OK) return s;
+  if ((s = run_attention(*p, Q, K, V, mask, p->c_h, O, lse, st, nullptr, nullptr, workspace, true)) != US_OK)
+    return s;
   g_prof.mark(call, 4, st);
   if (p->flags & US_FLAG_SYNC_CHECK) return sync_check(*p, workspace, st, "unisparse_attn");
   return US_OK;

@@ -93,6 +93,15 @@ inline long long work_items(const AttnArgs& a) {
   return (long long)a.B * a.H * ((a.N + 3) / 4);
 }
 
+// The automatic kernel choice for a mask (a.sel_pairs set): the M = 64 chains of
+// attention64.cu when under 40 % of the causal (i, j <= i) block pairs are selected, the
+// two-tile kernel otherwise. Measured crossover at C3 shapes (profiles/r02c/README.md):
+// attention64 0.92x the time of attn_kernel at 10.6 % selected, 0.98x at 32 %, 1.05x at 62 %.
+__device__ __forceinline__ bool m64_wins(const AttnArgs& a) {
+  const unsigned long long pairs = (unsigned long long)a.B * a.H * a.N * (a.N + 1) / 2;
+  return *a.sel_pairs * 5ull < pairs * 2ull;
+}
+
 __device__ __forceinline__ int last_block(const AttnArgs& a, const Groups& gr) {
   int jmax = -1;
   for (int k = 0; k < 4; ++k)

@@ -145,6 +145,11 @@ struct AttnArgs {
   uint32_t* err;        // device error word (nullable): |= 4 non-causal bit, |= 8 empty row
   int32_t* first_bad;   // first offending mask row (atomicMin; nullable with err)
   int noncausal;        // 1: dense_attention(in, causal = false): all N key blocks, no diagonal mask
+  int32_t* items;       // attention64.cu: work-item table [B*H_kv][ceil(G*N/4)][4] of (h << 16 | i), -1 = none
+                        // (nullable: the fixed decode_item order)
+  unsigned long long* sel_pairs;  // automatic choice (nullable = off): selected (i, j <= i) pairs of the mask,
+                                  // summed by attn64_items_kernel; both kernels are launched and each CTA
+                                  // exits unless attn::m64_wins(a) picks its kernel (attn_common.cuh)
 };
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);
@@ -155,6 +160,13 @@ us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUte
 // tmQ: 2-D map (box 64 rows x 64); tmK / tmV: 3-D rows-chunked maps (box 64 rows).
 us_status launch_attention_tp(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                               const CUtensorMap& tmV, cudaStream_t st);
+
+// One M = 64 UMMA chain per query group (attention64.cu): same work decomposition and
+// union list as launch_attention, two groups per set of TMEM columns at lane offsets 0 / 16.
+// tmK / tmV: 3-D rows-chunked maps (box 64 rows).
+us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st);
+// int32 entries of the attention64 work-item table (a.items) for these dims
+long long attention64_item_entries(int B, int H, int H_kv, int N);
 
 // Key-major variant (attention_kt.cu, d_k = 128): one query group per work item,
 // M = 128 = a pair of its own selected key blocks (no union rows); persistent CTAs.

@@ -288,9 +288,10 @@ def test_sparse_attention_rejects_malformed_masks():
 def test_attention_impls_agree(H, H_kv, d):
     """attention.cu (64-key steps, two tiles per CTA) and the calibration variants —
     attention2.cu (128-key steps, one tile per CTA), the one-tile attention.cu, the
-    key-major attention_kt.cu and the decoupled-softmax attention_tp.cu (P in TMEM,
-    double-buffered logits, split K / V rings) — on the same random masks, odd union
-    lengths included: all equal the fp64 oracle within the bf16 tolerance."""
+    key-major attention_kt.cu, the decoupled-softmax attention_tp.cu (P in TMEM,
+    double-buffered logits, split K / V rings) and the M = 64 chains of attention64.cu —
+    on the same random masks, odd union lengths included: all equal the fp64 oracle
+    within the bf16 tolerance."""
     import ctypes
     rng = np.random.default_rng(H * 100 + d)
     B, L = 2, 1024
@@ -302,7 +303,7 @@ def test_attention_impls_agree(H, H_kv, d):
     bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
     with us().api.calibration() as lib:  # the variants live in the calibration build
         try:
-            for impl in ((5, 4, 3, 2, 1) if d == 128 else (5, 3, 2, 1)):
+            for impl in ((6, 5, 4, 3, 2, 1) if d == 128 else (6, 5, 3, 2, 1)):
                 assert lib.us_set_attention_impl(impl) == 0
                 Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
                 Og = Og.float().cpu().numpy()
@@ -314,6 +315,35 @@ def test_attention_impls_agree(H, H_kv, d):
                     assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
         finally:
             lib.us_set_attention_impl(0)
+
+
+@pytest.mark.parametrize("density", [0.08, 0.3, 0.5, 0.9])
+@pytest.mark.parametrize("H,H_kv,d", [(8, 2, 128), (6, 3, 64)])
+def test_automatic_choice_follows_the_density_gate(density, H, H_kv, d):
+    """impl 0 with a mask launches attention64.cu and attention.cu; the device-side gate
+    (attn_common.cuh m64_wins: under 40 % of the causal block pairs selected) lets exactly
+    one of them write O. The automatic output must equal, bit for bit, the forced run of
+    the kernel the rule picks on the host-counted density."""
+    rng = np.random.default_rng(int(density * 100) + H)
+    B, L = 2, 2048
+    N = L // 64
+    Q, K, V = (to_dev_bf16(x) for x in _rand_qkv(rng, B, H, H_kv, L, d))
+    mask = rng.random((B, H, N, N)) < density
+    mask &= np.tril(np.ones((N, N), bool))
+    mask[..., np.arange(N), np.arange(N)] = True
+    bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
+    frac = mask.sum() / (B * H * N * (N + 1) / 2)
+    out = {}
+    try:
+        for impl in (0, 1, 6):
+            _set_impl(impl)
+            Og, lseg = us().block_sparse_attention(Q, K, V, bits)
+            out[impl] = (Og.clone(), lseg.clone())
+    finally:
+        _set_impl(0)
+    want = 6 if frac * 5 < 2 else 1
+    assert torch.equal(out[0][0], out[want][0]), (frac, want)
+    assert torch.equal(out[0][1], out[want][1]), (frac, want)
 
 
 def test_product_library_has_no_calibration_variants():
