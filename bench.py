@@ -624,19 +624,30 @@ def main():
     hbm, tf_burst, tf_sust, peak_src = peaks()
     flops_attn = selected * 4 * 64 * 64 * d
     dominant = max(stage_ms.items(), key=lambda kv: kv[1])[0]
-    issued_attn = (tile_eff["issued_tile_steps"] * 2 * 64 * 64 * 4 * d) if tile_eff else None
+    # the kernel the device-side density gate runs (attn_common.cuh m64_wins, per call =
+    # per shard here): attention64.cu under 40 % of the causal block pairs selected
+    m64 = selected * 5 < causal * 2
+    if m64:
+        # one M = 64 UMMA chain per query group: every issued row is a selected one, and an
+        # M = 64 MMA occupies the tensor pipe for the cycles of M = 128 (B300_MICROARCH.md,
+        # profiles/r02c/m64_probes.txt), so issued-equivalent = 2 x useful
+        issued_attn, rows_useful = selected * 2 * 64 * 64 * 4 * d, 0.5
+    else:
+        # M = 128 tiles of two query groups run S / P.V for the union of their selections
+        issued_attn = (tile_eff["issued_tile_steps"] * 2 * 64 * 64 * 4 * d) if tile_eff else None
+        rows_useful = tile_eff["rows_useful_fraction"] if tile_eff else None
     if dominant == "attention":
         achieved = flops_attn / (stage_ms["attention"] * 1e-3) / 1e12
-        roof = {"kernel": "attn_kernel (tcgen05 block-sparse FA)", "bound": "tensor", "achieved": achieved,
+        roof = {"kernel": ("attn64_kernel (tcgen05 M=64 chains, block-sparse FA)" if m64 else
+                           "attn_kernel (tcgen05 block-sparse FA)"), "bound": "tensor", "achieved": achieved,
                 "peak": tf_sust, "unit": "TFLOP/s", "frac": achieved / tf_sust,
                 "algorithmic": "selected_blocks * 4 * S^2 * d (metrics.cpp:83-85)",
                 "issued_tflops": issued_attn / (stage_ms["attention"] * 1e-3) / 1e12 if issued_attn else None}
         if issued_attn:
-            # M = 128 UMMA tiles hold two 64-row query groups and run S / P.V for the union of
-            # their selections; an M = 64 MMA costs the cycles of M = 128, so the useful fraction
-            # is capped at rows_useful_fraction x the issued fraction (DESIGN.md §3 a6)
+            # an M = 64 MMA costs the cycles of M = 128, so the useful fraction is capped at
+            # rows_useful_fraction x the issued fraction (DESIGN.md §3 a6)
             roof["issued_frac"] = roof["issued_tflops"] / tf_sust
-            roof["rows_useful_fraction"] = tile_eff["rows_useful_fraction"]
+            roof["rows_useful_fraction"] = rows_useful
     else:
         Lq = L // 8
         fl = 2 * Lq * Lq * len(heads) * len(shard.batch) * d  # compressed_qk (metrics.cpp:60), post-softmax full square
@@ -671,7 +682,7 @@ def main():
                             "achieved_tflops": qk / (stage_ms["proxy"] * 1e-3) / 1e12,
                             "issued_tflops": 3 * qk / (stage_ms["proxy"] * 1e-3) / 1e12, "peak_tflops": tf_sust,
                             "mufu_floor_ms": n_exp_proxy / mufu_per_s * 1e3}
-    if tile_eff:
+    if issued_attn:
         useful_exp = selected * 64 * 64
         stage_roofs["attention"]["mufu_floor_ms"] = useful_exp * 7 / 8 / mufu_per_s * 1e3
         stage_roofs["attention"]["tensor_floor_ms_issued"] = (issued_attn / (tf_sust * 1e12)) * 1e3

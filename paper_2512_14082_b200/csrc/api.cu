@@ -222,7 +222,7 @@ Ws layout(const us_params& p, bool scores_region = false) {
   const size_t n64 = size_t(g.L) / kGpuBlock;
   w.mask64 = g.S != kGpuBlock ? take(4 * size_t(g.B) * g.H * n64 * ((n64 + 31) / 32)) : 0;
   // attention64.cu work-item table (groups sorted by selected-block count)
-  w.items = take(4 * size_t(attention64_item_entries(g.B, g.H, g.H_kv, int(n64))) + 16);  // + the sel_pairs counter
+  w.items = take(attention64_ws_bytes(g.B, g.H, g.H_kv, int(n64)));
   w.total = o;
   return w;
 }
@@ -581,18 +581,19 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   a.one_tile = impl == 3 ? 1 : 0;
   if (impl == 5) return launch_attention_tp(a, tQ, tK3, tV3, st);
 #endif
-  if (impl == 6 && mask) {  // forced
+  if (mask && items && (impl == 6 || impl == 0)) {
+    const long long entries = attention64_item_entries(g.B, g.H, g.H_kv, g.N);
     a.items = items;
-    return launch_attention64(a, tK3, tV3, st);
-  }
-  if (impl == 0 && mask && items) {
+    a.row_counts = items + entries + 4;
+    if (impl == 6) return launch_attention64(a, tK3, tV3, st);  // forced
     // automatic: the density is known on the device only; attention64's pre-pass counts the
     // selected pairs and each kernel's CTAs exit unless attn::m64_wins picks that kernel
-    a.items = items;
-    a.sel_pairs = reinterpret_cast<unsigned long long*>(
-        items + attention64_item_entries(g.B, g.H, g.H_kv, g.N));
+    a.sel_pairs = reinterpret_cast<unsigned long long*>(items + entries);
     if ((s = launch_attention64(a, tK3, tV3, st)) != US_OK) return s;
     a.items = nullptr;
+    a.row_counts = nullptr;
+  } else if (mask && impl == 6) {
+    return launch_attention64(a, tK3, tV3, st);  // forced, no workspace: the fixed decode order
   }
   return launch_attention(a, tQ, tK3, tV3, st);
 }

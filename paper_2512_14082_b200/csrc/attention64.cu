@@ -378,6 +378,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// Selected key blocks j <= i of every mask row (one warp per row, lanes over the row's
+// words), and their total over the heads (a.sel_pairs, the density gate's input).
+__global__ void __launch_bounds__(256) attn64_counts_kernel(AttnArgs a) {
+  __shared__ unsigned part[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long rows = (long long)a.B * a.planes * a.N;
+  const long long r = (long long)blockIdx.x * 8 + warp;
+  unsigned n = 0;
+  if (r < rows) {
+    const int i = int(r % a.N);
+    const uint32_t* row = a.mask + r * a.W;
+    for (int w = lane; w <= (i >> 5); w += 32) {
+      uint32_t word = row[w];
+      const int hi = i - (w << 5);
+      if (hi < 31) word &= (2u << hi) - 1u;
+      n += __popc(word);
+    }
+    n = __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0) a.row_counts[r] = int32_t(n);
+  }
+  if (a.sel_pairs) {
+    if (lane == 0) part[warp] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int k = 0; k < 8; ++k) t += part[k];
+      if (t) atomicAdd(a.sel_pairs, t * (unsigned long long)a.heads_per_plane);
+    }
+  }
+}
+
 // Work items for the four chains of a CTA: the G * N query groups of one (batch, KV head),
 // ordered by their number of selected key blocks (heaviest first, counting sort), packed
 // four at a time — so a CTA's chains have near-equal lengths (a CTA lasts as long as its
@@ -392,28 +423,11 @@ __global__ void __launch_bounds__(1024) attn64_items_kernel(AttnArgs a) {
   int32_t* out = a.items + (long long)bk * per_kv * 4;
   for (int c = threadIdx.x; c < N + 2; c += blockDim.x) hist[c] = 0;
   __syncthreads();
-  auto count_of = [&](int e) {  // selected blocks j <= i of group e = (head, query block)
-    const int h = kvh * G + e / N, i = e % N;
-    const uint32_t* row = a.mask + ((long long)(b * a.planes + h / a.heads_per_plane) * N + i) * a.W;
-    int n = 0;
-    for (int w = 0; w <= (i >> 5); ++w) {
-      uint32_t word = row[w];
-      const int hi = i - (w << 5);
-      if (hi < 31) word &= (2u << hi) - 1u;
-      n += __popc(word);
-    }
-    return n;
+  auto count_of = [&](int e) {  // group e = (head kvh * G + e / N, query block e % N)
+    const int h = kvh * G + e / N;
+    return int(a.row_counts[(long long)(b * a.planes + h / a.heads_per_plane) * N + e % N]);
   };
-  int mine = 0;
-  for (int e = threadIdx.x; e < G * N; e += blockDim.x) {
-    const int n = count_of(e);
-    atomicAdd(&hist[n], 1);
-    mine += n;
-  }
-  if (a.sel_pairs) {
-    mine = __reduce_add_sync(0xffffffffu, unsigned(mine));
-    if ((threadIdx.x & 31) == 0) atomicAdd(a.sel_pairs, (unsigned long long)mine);
-  }
+  for (int e = threadIdx.x; e < G * N; e += blockDim.x) atomicAdd(&hist[count_of(e)], 1);
   __syncthreads();
   if (threadIdx.x == 0) {  // descending exclusive starts (counts 0..N)
     int run = 0;
@@ -440,6 +454,9 @@ us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensor
   long long items = attn::work_items(a);
   if (a.items) {
     if (a.sel_pairs) US_CUDA_TRY(cudaMemsetAsync(a.sel_pairs, 0, sizeof(unsigned long long), st), "sel_pairs reset");
+    const long long rows = (long long)a.B * a.planes * a.N;
+    attn64_counts_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(a);
+    US_LAUNCH_CHECK("attn64_counts_kernel");
     attn64_items_kernel<<<unsigned(a.B * a.H_kv), 1024, (a.N + 2) * 4, st>>>(a);
     US_LAUNCH_CHECK("attn64_items_kernel");
     items = (long long)a.B * a.H_kv * ((a.H / a.H_kv * a.N + 3) / 4);
@@ -453,6 +470,10 @@ us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensor
 
 long long attention64_item_entries(int B, int H, int H_kv, int N) {
   return (long long)B * H_kv * ((H / H_kv * N + 3) / 4) * 4;
+}
+
+size_t attention64_ws_bytes(int B, int H, int H_kv, int N) {
+  return 4 * size_t(attention64_item_entries(B, H, H_kv, N)) + 16 + 4 * size_t(B) * H * N;
 }
 
 us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st) {
