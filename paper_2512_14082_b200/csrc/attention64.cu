@@ -21,17 +21,48 @@
 // * Each group's softmax is four warps (one per lane quarter); a warp reads its 16 rows with
 //   the 16x32bx2 TMEM shape — two threads per row, 32 key columns each; the row max is one
 //   shuffle between the two.
-// K/V tiles of 64 keys arrive by TMA once per union position (all four groups' selected
-// blocks, ascending) into a ring shared by the four chains; the producer releases each
-// position on behalf of the chains whose group skips it, so a chain only holds ring stages
-// of its own positions.
+// * K/V tiles of 64 keys arrive by TMA in step-major order (round k: the k-th selected block
+//   of chain 0, 1, 2, 3) into a K ring and a V ring shared by the four chains, so the rings
+//   hold the next steps of every chain (see the producers); four producer warps issue the
+//   copies, as one issuing warp caps at ~20-29 B/clk (tools/tma_probe.cu).
+// * The four chains' causal mask rows live in shared memory (the producers' walk); all
+//   shared memory is dynamic (the rows' size follows W).
 //
-// Warps (672 threads): 0 list builder + TMA producer, 1-3 and 20 MMA issuers of groups
-// 0-3 (warp 1 owns TMEM), 4-19 softmax (warp 4 + 4 g + q: group g, lane quarter q).
+// Warps (768 threads): 0 row loader + K producer, 21 K producer, 22-23 V producers, 1-3 and 20
+// MMA issuers of groups 0-3 (warp 1 owns TMEM), 4-19 softmax (warp 4 + 4 g + q: group g, lane
+// quarter q).
 #include "attn_common.cuh"
 #include "host_util.hpp"
 #include "kernels.cuh"
 #include "ptx.cuh"
+
+#ifndef US_ATTN_TRACE
+#define US_ATTN_TRACE 0
+#endif
+#if US_ATTN_TRACE
+// clock64 step timeline of one CTA (tools/a64_trace.py): [group][own step][event]; event 7 of a
+// group step = its load index (a value, not a time); [4][load][0 / 1] = K / V load issued
+__device__ long long g_a64_trace[5 * 4096 * 8];  // [group 0-3 | 4 = producer]
+__device__ int g_a64_trace_cta = -1;
+#define A64_STAMP(g, k, e) \
+  do { if (traced && (k) < 4096) g_a64_trace[(((g) * 4096) + (k)) * 8 + (e)] = clock64(); } while (0)
+#else
+#define A64_STAMP(g, k, e) do { } while (0)
+#endif
+
+// ring split (stages of 16 KB at d = 128; twice as many 8 KB stages at d = 64) and the
+// number of the four producer warps that issue K (the rest issue V). Measured at C3
+// (profiles/r02d): K6/V6 with 2 + 2 producers 5.3-5.5 ms at 64K gain 9; K8/V4 5.5-5.6,
+// K7/V5 5.7-5.8, one K producer (3 V) 6.2-7.0.
+#ifndef US_A64_KS
+#define US_A64_KS 6
+#endif
+#ifndef US_A64_VS
+#define US_A64_VS 6
+#endif
+#ifndef US_A64_KPROD
+#define US_A64_KPROD 2
+#endif
 
 namespace us {
 namespace {
@@ -41,36 +72,64 @@ using attn::kMaxN;
 
 template <int D>
 struct A64Smem {
-  static constexpr int kST = D == 128 ? 5 : 10;  // K/V ring stages
+  // K ring: a K tile is held until its S retires; V ring: a V tile until its P.V retires
+  static constexpr int kKS = (D == 128 ? 1 : 2) * US_A64_KS;
+  static constexpr int kVS = (D == 128 ? 1 : 2) * US_A64_VS;
   static constexpr int kChunks = D / 64;
-  static constexpr int kKVBytes = kBS * D * 2;   // one of K / V per stage
-  static constexpr int kRingBytes = kST * 2 * kKVBytes;
+  static constexpr int kKVBytes = kBS * D * 2;   // one K or V tile of 64 keys
+  static constexpr int kRingBytes = (kKS + kVS) * kKVBytes;  // K stages, then V stages
   static constexpr int kPBytes = 64 * kBS * 2;   // per group: 64 rows x 64 keys bf16, SWIZZLE_128B
-  static constexpr int kBytes = kRingBytes + 4 * kPBytes;
+  // control block (barriers, counters) after the P tiles, then the four mask rows
+  struct Ctl {
+    uint64_t bar_q[4], bar_kfull[kKS], bar_kempty[kKS], bar_vfull[kVS], bar_vempty[kVS], bar_sfull[4], bar_sfree[4],
+        bar_pfull[4], bar_pvdone[4], bar_ofull[4];
+    uint32_t tmem_base;
+    int k_issued, v_issued;  // loads of the sequence whose K / V the producer has issued
+    int n_own[4];            // own steps (selected blocks j <= i) of each chain
+  };
+  static constexpr int kCtlOff = kRingBytes + 4 * kPBytes;
+  static constexpr int kRowsOff = kCtlOff + (int(sizeof(Ctl)) + 15) / 16 * 16;
+  // dynamic bytes for W mask words per row; ALL the kernel's shared memory is dynamic (no
+  // static __shared__), so the base is the window base, 1024-aligned (checked in the kernel)
+  static constexpr int bytes(int W) { return kRowsOff + 16 * W; }
 };
 
 constexpr uint32_t kTS = 0, kTO = 64, kTQ = 192;
-constexpr int kThreads = 21 * 32;
+constexpr int kThreads = 24 * 32;
 constexpr int kPolyFrom = 28;  // columns >= this of each 32-column half of an off-diagonal block: FMA-pipe exp2
 
 __device__ __forceinline__ int issuer_group(int warp) { return warp == 20 ? 3 : warp - 1; }
+
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn64_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const AttnArgs a) {
   using SL = A64Smem<D>;
-  constexpr int kST = SL::kST;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q[4], bar_kvfull[kST], bar_kvempty[kST], bar_sfull[4], bar_sfree[4], bar_pfull[4],
-      bar_pvdone[4], bar_ofull[4];
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ attn::ListsCore ls;
-  __shared__ int kv_issued;  // union positions whose K/V load the producer has issued
+  constexpr int kKS = SL::kKS, kVS = SL::kVS;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u)) __trap();  // SWIZZLE_128B tiles need 1024-B alignment
+  auto& ctl = *reinterpret_cast<typename SL::Ctl*>(smem + SL::kCtlOff);
+  auto& bar_q = ctl.bar_q;
+  auto& bar_kfull = ctl.bar_kfull;
+  auto& bar_kempty = ctl.bar_kempty;
+  auto& bar_vfull = ctl.bar_vfull;
+  auto& bar_vempty = ctl.bar_vempty;
+  auto& bar_sfull = ctl.bar_sfull;
+  auto& bar_sfree = ctl.bar_sfree;
+  auto& bar_pfull = ctl.bar_pfull;
+  auto& bar_pvdone = ctl.bar_pvdone;
+  auto& bar_ofull = ctl.bar_ofull;
+  auto& k_issued = ctl.k_issued;
+  auto& v_issued = ctl.v_issued;
+  auto& n_own = ctl.n_own;
+  uint32_t* const mrow = reinterpret_cast<uint32_t*>(smem + SL::kRowsOff);  // [4][W]: causal rows
 
   if (a.sel_pairs && !attn::m64_wins(a)) return;  // the mask is dense enough for attn_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if US_ATTN_TRACE
+  const bool traced = int(blockIdx.x) == g_a64_trace_cta;
+#endif
   const int G = a.H / a.H_kv;
   attn::Groups gr;
   int kvh;
@@ -90,7 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     gr = attn::decode_item(a, blockIdx.x);
     kvh = gr.h[0] / G;
   }
-  const int jmax = attn::last_block(a, gr);
+  // mask row of chain g (its selected key blocks; read through L1 by the cursors below)
+  auto row_of = [&](int g) {
+    return a.mask + ((long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + gr.i[g]) * a.W;
+  };
 
   if (threadIdx.x == 32) {
     for (int g = 0; g < 4; ++g) {
@@ -101,43 +163,114 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_pvdone[g], 1);
       mbar_init(&bar_ofull[g], 1);
     }
-    for (int s = 0; s < kST; ++s) {
-      mbar_init(&bar_kvfull[s], 1);
-      mbar_init(&bar_kvempty[s], 4);  // every chain releases every union position
+    for (int s = 0; s < kKS; ++s) {
+      mbar_init(&bar_kfull[s], 1);
+      mbar_init(&bar_kempty[s], 1);  // each load belongs to one chain
     }
-    kv_issued = 0;
+    for (int s = 0; s < kVS; ++s) {
+      mbar_init(&bar_vfull[s], 1);
+      mbar_init(&bar_vempty[s], 1);
+    }
+    k_issued = v_issued = 0;
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&tmem_base_sh, 512);
-  // (no pairing: union bit 12 + g is group g)
-  if (warp == 0) attn::build_lists(a, gr, jmax, false, ls, nullptr);
+  if (warp == 1) tmem_alloc(&ctl.tmem_base, 512);
+  if (warp == 0) {
+    // the causal rows of the four chains -> shared memory, own steps of each chain (their
+    // popcounts) and the asynchronous data-error report (the reference throws,
+    // attention.cpp:106-108, 127-129): a non-causal bit anywhere in the row, or an empty
+    // causal prefix
+    for (int g = 0; g < 4; ++g) {
+      unsigned c = 0, bad = 0;
+      const uint32_t* src = row_of(g);
+      const int ig = gr.i[g];
+      for (int w = lane; w < a.W; w += 32) {
+        const uint32_t word = gr.en[g] ? src[w] : 0u;
+        const int lo = w << 5;
+        const uint32_t keep = lo > ig ? 0u : (ig - lo >= 31 ? ~0u : (2u << (ig - lo)) - 1u);
+        bad |= word & ~keep;
+        c += __popc(word & keep);
+        mrow[g * a.W + w] = word & keep;
+      }
+      c = __reduce_add_sync(0xffffffffu, c);
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        n_own[g] = int(c);
+        if (a.err && gr.en[g] && (bad || c == 0)) {
+          atomicOr(a.err, bad ? 4u : 8u);
+          atomicMin(a.first_bad, int32_t((src - a.mask) / a.W));
+        }
+      }
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  const int T = ls.n_steps;
+  const uint32_t tmem = ctl.tmem_base;
+  const int n0 = n_own[0], n1 = n_own[1], n2 = n_own[2], n3 = n_own[3];
+  // index of chain g's own step k in the load sequence (round k: chains 0-3 in order, a
+  // chain with fewer than k + 1 steps skipped)
+  auto seq_index = [&](int g, int k) {
+    return min(k, n0) + min(k, n1) + min(k, n2) + min(k, n3) + (g > 0 && n0 > k) + (g > 1 && n1 > k) +
+           (g > 2 && n2 > k);
+  };
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp == 0 || warp >= 21) {
+    // ------------------------------------------------------------ TMA producers
+    // The load sequence is step-major: round k loads the k-th own block of chain 0, 1, 2, 3
+    // (seq_index). The chains of a CTA have near-equal lengths (the sorted work items) and
+    // advance together, so the ring windows hold the next steps of every chain; a
+    // union-ordered sequence (ascending j) lets a chain whose blocks sit early in j fill the
+    // ring while the others starve. A block two chains selected is loaded twice.
+    // K and V are two sequences (a K tile is only held until its S retires, so K runs ahead):
+    // K(u) once K stage u % kKS is free, V(u) once V stage u % kVS is. One warp issues only
+    // ~20-29 B/clk of bulk / tensor copies however deep its ring (tools/tma_probe.cu: the
+    // copies of one issuing warp proceed one at a time; four issuing warps reach the
+    // ~70 B/clk/SM L2 -> SMEM ceiling), so each sequence is dealt round-robin to two warps
+    // (K: warps 0, 21; V: warps 22, 23). Arming a load (stage free, expect_tx, the issued
+    // count) stays in sequence order; the copies run in parallel.
+    const int pw = warp == 0 ? 0 : warp - 20;  // 0 .. kKProd - 1: K producers; the rest V
+    constexpr int kKProd = US_A64_KPROD;
+    const bool is_v = pw >= kKProd;
+    const int np = is_v ? 4 - kKProd : kKProd, me = is_v ? pw - kKProd : pw;
     if (elect_one()) {
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
+      if (pw == 0) {
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+      }
       const uint64_t pol_kv = policy_evict_last();
       const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
-      for (int t = 0; t < T; ++t) {
-        const int j = int(ls.steps[t] & 0xFFFu);
-        const int s = t % kST;
-        if (t >= kST) mbar_wait(&bar_kvempty[s], ((t / kST) + 1) & 1);
-        uint8_t* sk = smem + s * 2 * SL::kKVBytes;
-        uint8_t* sv = sk + SL::kKVBytes;
-        mbar_arrive_expect_tx(&bar_kvfull[s], 2 * SL::kKVBytes);
-        tma_load_3d_hint(sk, &tmK, &bar_kvfull[s], 0, kvrow0 + j * kBS, 0, pol_kv);
-        tma_load_3d_hint(sv, &tmV, &bar_kvfull[s], 0, kvrow0 + j * kBS, 0, pol_kv);
-        // a chain whose group skips this position releases it right away (the producer
-        // arrives for it): a chain only ever holds the stages of its own positions
-        for (int g = 0; g < 4; ++g)
-          if (((ls.steps[t] >> (12 + g)) & 1u) == 0u) mbar_arrive(&bar_kvempty[s]);
-        *reinterpret_cast<volatile int*>(&kv_issued) = t + 1;
+      const int total = n0 + n1 + n2 + n3;
+      const int nmax = max(max(n0, n1), max(n2, n3));
+      const CUtensorMap* tm = is_v ? &tmV : &tmK;
+      const int nst = is_v ? kVS : kKS;
+      uint64_t* full = is_v ? bar_vfull : bar_kfull;
+      uint64_t* empty = is_v ? bar_vempty : bar_kempty;
+      int* issued = is_v ? &v_issued : &k_issued;
+      uint8_t* ring = smem + (is_v ? kKS : 0) * SL::kKVBytes;
+      // walk of the sequence: (round k, chain g) and a bit cursor per chain
+      int k = 0, g = 0, w[4] = {0, 0, 0, 0};
+      uint32_t bits[4];
+      for (int c = 0; c < 4; ++c) bits[c] = mrow[c * a.W];
+      for (int u = 0; u < total; ++u) {
+        while (k < nmax && k >= n_own[g]) {
+          if (++g == 4) { g = 0; ++k; }
+        }
+        while (bits[g] == 0u) bits[g] = mrow[g * a.W + ++w[g]];
+        const int j = (w[g] << 5) + __ffs(bits[g]) - 1;
+        bits[g] &= bits[g] - 1u;
+        if (++g == 4) { g = 0; ++k; }
+        if (u % np != me) continue;  // another producer's load of this sequence
+        const int s = u % nst;
+        while (*reinterpret_cast<const volatile int*>(issued) < u) {
+        }
+        // (load u - nst armed => load u - 2 nst released: the parity wait is within one phase)
+        if (u >= nst) mbar_wait(&empty[s], ((u / nst) + 1) & 1);
+        mbar_arrive_expect_tx(&full[s], SL::kKVBytes);
+        __threadfence_block();
+        *reinterpret_cast<volatile int*>(issued) = u + 1;
+        tma_load_3d_hint(ring + s * SL::kKVBytes, tm, &full[s], 0, kvrow0 + j * kBS, 0, pol_kv);
+        A64_STAMP(4, u, is_v ? 1 : 0);  // (trace) K / V load u issued
       }
     }
     __syncwarp();
@@ -148,24 +281,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_o = idesc_f16(64, D, /*bf16*/ 1, false, /*V MN-major*/ true);
     const uint32_t tb = tmem + (g >> 1) * 256 + (uint32_t((g & 1) * 16) << 16);
     const uint32_t sP = smem_u32(smem + SL::kRingBytes + g * SL::kPBytes);
-    // next union position at or after p that group g selected (T past the last)
-    auto own_from = [&](int p) {
-      while (p < T && ((ls.steps[p] >> (12 + g)) & 1u) == 0u) ++p;
-      return p;
+    const int n = n_own[g];
+    // K (V) of load u: a parity wait is only meaningful within one phase of the barrier, so
+    // the chain waits on kfull(u) only once the producer has ISSUED load u — which implies
+    // load u - kKS has landed (its release needed it); the barrier cannot be ahead (this
+    // chain holds u).
+    auto wait_k = [&](int u) {
+      while (*reinterpret_cast<const volatile int*>(&k_issued) <= u) __nanosleep(20);
+      mbar_wait(&bar_kfull[u % kKS], (u / kKS) & 1);
     };
-    // K/V of own position tt: a parity wait is only meaningful within one phase of the
-    // barrier, and the stage advances on positions this chain skips, so the chain waits on
-    // kvfull(tt) only once the producer has ISSUED load tt — which implies load tt - kST has
-    // landed (its release needed it); the barrier cannot be ahead (this chain holds tt).
-    auto wait_kv = [&](int tt) {
-      while (*reinterpret_cast<const volatile int*>(&kv_issued) <= tt) __nanosleep(20);
-      mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
+    auto wait_v = [&](int u) {
+      while (*reinterpret_cast<const volatile int*>(&v_issued) <= u) __nanosleep(20);
+      mbar_wait(&bar_vfull[u % kVS], (u / kVS) & 1);
     };
-    auto issue_s = [&](int tt) {
-      wait_kv(tt);
+    auto issue_s = [&](int kk) {
+      const int u = seq_index(g, kk);
+      A64_STAMP(g, kk, 3);  // S(kk) wants to issue
+      wait_k(u);
+      A64_STAMP(g, kk, 4);  // ... its K landed: issued
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sK = smem_u32(smem + (tt % kST) * 2 * SL::kKVBytes);
+        const uint32_t sK = smem_u32(smem + (u % kKS) * SL::kKVBytes);
 #pragma unroll
         for (int kc = 0; kc < SL::kChunks; ++kc)
 #pragma unroll
@@ -174,44 +310,40 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_f16_ts(tb + kTS, tb + kTQ + (kc * 4 + ks) * 8, bd, idesc_s, (kc | ks) != 0);
           }
         umma_commit(&bar_sfull[g]);
+        umma_commit(&bar_kempty[u % kKS]);
       }
       __syncwarp();
     };
     mbar_wait(&bar_q[g], 0);  // Q rows of group g are in TMEM
     tc_fence_after();
-    int t = own_from(0);
-    if (t < T) issue_s(t);
-    int k = 0;
-    while (t < T) {
-      const int tn = own_from(t + 1);
-      // S(k+1) early (right after the softmax has loaded S(k)) only when tn lies within kST
-      // positions of t: its stage then last held a position before t, which every chain
-      // has released or will release without waiting on this one (no cycle of chains
-      // waiting on each other's P.V); otherwise after P.V(k)
+    if (n > 0) issue_s(0);
+    for (int k = 0; k < n; ++k) {
+      // S(k+1) right after the softmax has loaded S(k), when its K has landed (a non-blocking
+      // probe: P.V(k) is not held up by a late K); otherwise after P.V(k). (Blocking here would
+      // also be safe: K(u) needs only the S MMAs of earlier loads, never a P.V.)
       mbar_wait(&bar_sfree[g], k & 1);
-      // ... or, further ahead, when its K/V has already landed (a non-blocking probe: a
-      // chain never blocks on a stage before its own P.V(k) could free one)
-      const bool early =
-          tn < T && (tn - t < kST || (*reinterpret_cast<const volatile int*>(&kv_issued) > tn &&
-                                      mbar_test_wait(&bar_kvfull[tn % kST], (tn / kST) & 1)));
-      if (early) issue_s(tn);
+      const int u1 = k + 1 < n ? seq_index(g, k + 1) : -1;
+      const bool early = u1 >= 0 && *reinterpret_cast<const volatile int*>(&k_issued) > u1 &&
+                         mbar_test_wait(&bar_kfull[u1 % kKS], (u1 / kKS) & 1);
+      if (early) issue_s(k + 1);
+      const int u = seq_index(g, k);
       mbar_wait(&bar_pfull[g], k & 1);  // P(k) of the group's 64 rows is in SMEM
+      wait_v(u);
+      A64_STAMP(g, k, 5);  // P(k) seen and V landed: P.V(k) issued
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sV = smem_u32(smem + (t % kST) * 2 * SL::kKVBytes + SL::kKVBytes);
+        const uint32_t sV = smem_u32(smem + (kKS + u % kVS) * SL::kKVBytes);
 #pragma unroll
         for (int ks = 0; ks < kBS / 16; ++ks) {
           const uint64_t ad = sdesc_sw128(sP + ks * 32, 16, 1024);
           const uint64_t bd = sdesc_sw128(sV + ks * 16 * 128, kBS * 128, 1024);
           umma_f16_ss(tb + kTO, ad, bd, idesc_o, (k > 0 || ks > 0) ? 1u : 0u);
         }
-        umma_commit(&bar_kvempty[t % kST]);
+        umma_commit(&bar_vempty[u % kVS]);
         umma_commit(&bar_pvdone[g]);
       }
       __syncwarp();
-      if (!early && tn < T) issue_s(tn);
-      t = tn;
-      ++k;
+      if (!early && u1 >= 0) issue_s(k + 1);
     }
     if (elect_one()) umma_commit(&bar_ofull[g]);
     __syncwarp();
@@ -250,16 +382,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_q[g]);
     }
-    auto own_from = [&](int p) {
-      while (p < T && ((ls.steps[p] >> (12 + g)) & 1u) == 0u) ++p;
-      return p;
-    };
-    int k = 0;
-    int t = own_from(0);
-    while (t < T) {
-      const int j = int(ls.steps[t] & 0xFFFu);
-      const int tn = own_from(t + 1);  // (independent shared loads: overlap the wait below)
+    const int n = n_own[g];
+    // own blocks ascend and end at j <= i: only the last can be the diagonal block
+    const bool diag_sel = n > 0 && ((mrow[g * a.W + (ig >> 5)] >> (ig & 31)) & 1u);
+    for (int k = 0; k < n; ++k) {
+      if (threadIdx.x % 128 == 0) A64_STAMP(g, k, 0);  // softmax (quarter 0) wants S(k)
+#if US_ATTN_TRACE
+      if (traced && threadIdx.x % 128 == 0 && k < 4096) g_a64_trace[((g * 4096) + k) * 8 + 7] = seq_index(g, k);
+#endif
       mbar_wait(&bar_sfull[g], k & 1);
+      if (threadIdx.x % 128 == 0) A64_STAMP(g, k, 1);  // S(k) seen
       tc_fence_after();
       float sv[32];
       {
@@ -273,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_sfree[g]);  // S(k+1) may now overwrite the S columns
       bool pv_prev_done = (k == 0);
-      const bool diag = (j == ig) && !a.noncausal;
+      const bool diag = diag_sel && k == n - 1;
       if (diag) {
 #pragma unroll
         for (int c = 0; c < 32; ++c)
@@ -335,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // P(k) -> the group's SWIZZLE_128B P tile (row r: 8 chunks of 16 B, this thread's 4);
       // P.V(k-1) must have consumed P(k-1) first
+      if (threadIdx.x % 128 == 0) A64_STAMP(g, k, 2);  // exponentials done
       if (!pv_prev_done) mbar_wait(&bar_pvdone[g], (k - 1) & 1);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -343,8 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_pfull[g]);
-      t = tn;
-      ++k;
+      if (threadIdx.x % 128 == 0) A64_STAMP(g, k, 6);  // P(k) handed off
     }
     // ---- epilogue: the row sum of both halves, this half of the O columns
     l += __shfl_xor_sync(0xffffffffu, l, 16);
@@ -447,9 +579,12 @@ __global__ void __launch_bounds__(1024) attn64_items_kernel(AttnArgs a) {
 
 template <int D>
 us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st) {
-  const int smem = A64Smem<D>::kBytes + 1024;  // + alignment slack
-  static std::atomic<uint64_t> attr_done{0};
-  if (us_status s = ensure_smem_attr(attn64_kernel<D>, smem, attr_done, "attn64_kernel smem attribute"); s != US_OK)
+  static_assert(A64Smem<D>::bytes(attn::kMaxW) <= 227 * 1024, "attn64_kernel shared memory");
+  const int smem = A64Smem<D>::bytes(a.W);
+  static std::atomic<uint64_t> attr_done{0};  // (the attribute: the largest W)
+  if (us_status s = ensure_smem_attr(attn64_kernel<D>, A64Smem<D>::bytes(attn::kMaxW), attr_done,
+                                     "attn64_kernel smem attribute");
+      s != US_OK)
     return s;
   long long items = attn::work_items(a);
   if (a.items) {
@@ -488,3 +623,10 @@ us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CU
 }
 
 }  // namespace us
+
+#if US_ATTN_TRACE
+extern "C" int us_debug_a64_trace(int cta, long long* host_out) {
+  if (host_out) return int(cudaMemcpyFromSymbol(host_out, ::g_a64_trace, sizeof(long long) * 5 * 4096 * 8));
+  return int(cudaMemcpyToSymbol(::g_a64_trace_cta, &cta, sizeof(int)));
+}
+#endif
