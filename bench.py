@@ -648,6 +648,13 @@ def main():
             # rows_useful_fraction x the issued fraction (DESIGN.md §3 a6)
             roof["issued_frac"] = roof["issued_tflops"] / tf_sust
             roof["rows_useful_fraction"] = rows_useful
+            # tensor-pipe occupancy from the MEASURED issue cost of each MMA (cycles per K = 16
+            # instruction, profiles/r02c/m64_probes.txt): S = Q K^T TS-mode N = 64 40.3; P.V SS-mode
+            # N = d: M = 64 84.3 (d = 128) / 52.3 (d = 64), M = 128 96.3 / 68.3
+            pv = {(True, 128): 84.3, (True, 64): 52.3, (False, 128): 96.3, (False, 64): 68.3}[(m64, d)]
+            steps = selected if m64 else tile_eff["issued_tile_steps"]
+            cyc = steps * ((d // 16) * 40.3 + 4 * pv)
+            roof["tensor_pipe_busy_est"] = cyc / (148 * (clk["sm_mhz"] or 1965.0) * 1e6 * stage_ms["attention"] * 1e-3)
     else:
         Lq = L // 8
         fl = 2 * Lq * Lq * len(heads) * len(shard.batch) * d  # compressed_qk (metrics.cpp:60), post-softmax full square

@@ -63,6 +63,11 @@ __device__ int g_a64_trace_cta = -1;
 #ifndef US_A64_KPROD
 #define US_A64_KPROD 2
 #endif
+// load order: 1 = union (ascending j over the four chains' blocks, a block two chains
+// selected loaded once), 0 = step-major (round k: the k-th block of each chain)
+#ifndef US_A64_UNION
+#define US_A64_UNION 1
+#endif
 
 namespace us {
 namespace {
@@ -86,6 +91,7 @@ struct A64Smem {
     uint32_t tmem_base;
     int k_issued, v_issued;  // loads of the sequence whose K / V the producer has issued
     int n_own[4];            // own steps (selected blocks j <= i) of each chain
+    int n_union;             // union positions (blocks any chain selected)
   };
   static constexpr int kCtlOff = kRingBytes + 4 * kPBytes;
   static constexpr int kRowsOff = kCtlOff + (int(sizeof(Ctl)) + 15) / 16 * 16;
@@ -107,6 +113,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const AttnArgs a) {
   using SL = A64Smem<D>;
   constexpr int kKS = SL::kKS, kVS = SL::kVS;
+  constexpr bool kUnion = US_A64_UNION != 0;
+  // union: every chain releases every position (the producer for the chains that skip it);
+  // step-major: each load belongs to one chain
+  constexpr int kEmptyCount = kUnion ? 4 : 1;
   extern __shared__ __align__(1024) uint8_t smem[];
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u)) __trap();  // SWIZZLE_128B tiles need 1024-B alignment
   auto& ctl = *reinterpret_cast<typename SL::Ctl*>(smem + SL::kCtlOff);
@@ -165,11 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kKS; ++s) {
       mbar_init(&bar_kfull[s], 1);
-      mbar_init(&bar_kempty[s], 1);  // each load belongs to one chain
+      mbar_init(&bar_kempty[s], kEmptyCount);
     }
     for (int s = 0; s < kVS; ++s) {
       mbar_init(&bar_vfull[s], 1);
-      mbar_init(&bar_vempty[s], 1);
+      mbar_init(&bar_vempty[s], kEmptyCount);
     }
     k_issued = v_issued = 0;
     fence_barrier_init();
@@ -202,6 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    __syncwarp();
+    unsigned nu = 0;
+    for (int w = lane; w < a.W; w += 32)
+      nu += __popc(mrow[w] | mrow[a.W + w] | mrow[2 * a.W + w] | mrow[3 * a.W + w]);
+    nu = __reduce_add_sync(0xffffffffu, nu);
+    if (lane == 0) ctl.n_union = int(nu);
   }
   tc_fence_before();
   __syncthreads();
@@ -213,6 +229,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto seq_index = [&](int g, int k) {
     return min(k, n0) + min(k, n1) + min(k, n2) + min(k, n3) + (g > 0 && n0 > k) + (g > 1 && n1 > k) +
            (g > 2 && n2 > k);
+  };
+  const int T = kUnion ? ctl.n_union : n0 + n1 + n2 + n3;  // loads of the sequence
+  auto union_word = [&](int w) {
+    return mrow[w] | mrow[a.W + w] | mrow[2 * a.W + w] | mrow[3 * a.W + w];
+  };
+  // union mode: chain g's own positions in ascending order, as union indices
+  struct OwnWalk {
+    int w = 0, base = 0;
+    uint32_t own = 0u, uni = 0u;
+  };
+  auto own_start = [&](int g) {
+    OwnWalk x;
+    x.own = mrow[g * a.W];
+    x.uni = union_word(0);
+    return x;
+  };
+  auto own_next = [&](OwnWalk& x, int g) {
+    while (x.own == 0u) {
+      x.base += __popc(x.uni);
+      ++x.w;
+      x.own = mrow[g * a.W + x.w];
+      x.uni = union_word(x.w);
+    }
+    const int b = __ffs(x.own) - 1;
+    x.own &= x.own - 1u;
+    return x.base + __popc(x.uni & ((1u << b) - 1u));
   };
 
   if (warp == 0 || warp >= 21) {
@@ -240,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint64_t pol_kv = policy_evict_last();
       const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
-      const int total = n0 + n1 + n2 + n3;
+      const int total = T;
       const int nmax = max(max(n0, n1), max(n2, n3));
       const CUtensorMap* tm = is_v ? &tmV : &tmK;
       const int nst = is_v ? kVS : kKS;
@@ -248,18 +290,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint64_t* empty = is_v ? bar_vempty : bar_kempty;
       int* issued = is_v ? &v_issued : &k_issued;
       uint8_t* ring = smem + (is_v ? kKS : 0) * SL::kKVBytes;
-      // walk of the sequence: (round k, chain g) and a bit cursor per chain
+      // walk of the sequence: step-major (round k, chain g) with a bit cursor per chain, or
+      // the union bits (word uw, remaining bits ub)
       int k = 0, g = 0, w[4] = {0, 0, 0, 0};
       uint32_t bits[4];
       for (int c = 0; c < 4; ++c) bits[c] = mrow[c * a.W];
+      int uw = 0;
+      uint32_t ub = union_word(0);
       for (int u = 0; u < total; ++u) {
-        while (k < nmax && k >= n_own[g]) {
+        int j;
+        if (kUnion) {
+          while (ub == 0u) ub = union_word(++uw);
+          j = (uw << 5) + __ffs(ub) - 1;
+          ub &= ub - 1u;
+        } else {
+          while (k < nmax && k >= n_own[g]) {
+            if (++g == 4) { g = 0; ++k; }
+          }
+          while (bits[g] == 0u) bits[g] = mrow[g * a.W + ++w[g]];
+          j = (w[g] << 5) + __ffs(bits[g]) - 1;
+          bits[g] &= bits[g] - 1u;
           if (++g == 4) { g = 0; ++k; }
         }
-        while (bits[g] == 0u) bits[g] = mrow[g * a.W + ++w[g]];
-        const int j = (w[g] << 5) + __ffs(bits[g]) - 1;
-        bits[g] &= bits[g] - 1u;
-        if (++g == 4) { g = 0; ++k; }
         if (u % np != me) continue;  // another producer's load of this sequence
         const int s = u % nst;
         while (*reinterpret_cast<const volatile int*>(issued) < u) {
@@ -267,6 +319,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (load u - nst armed => load u - 2 nst released: the parity wait is within one phase)
         if (u >= nst) mbar_wait(&empty[s], ((u / nst) + 1) & 1);
         mbar_arrive_expect_tx(&full[s], SL::kKVBytes);
+        if (kUnion) {
+          // a chain whose group skips this position releases it right away (the producer
+          // arrives for it): a chain only ever holds the stages of its own positions
+          const int wj = j >> 5;
+          const uint32_t bj = 1u << (j & 31);
+          for (int c = 0; c < 4; ++c)
+            if ((mrow[c * a.W + wj] & bj) == 0u) mbar_arrive(&empty[s]);
+        }
         __threadfence_block();
         *reinterpret_cast<volatile int*>(issued) = u + 1;
         tma_load_3d_hint(ring + s * SL::kKVBytes, tm, &full[s], 0, kvrow0 + j * kBS, 0, pol_kv);
@@ -294,8 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (*reinterpret_cast<const volatile int*>(&v_issued) <= u) __nanosleep(20);
       mbar_wait(&bar_vfull[u % kVS], (u / kVS) & 1);
     };
-    auto issue_s = [&](int kk) {
-      const int u = seq_index(g, kk);
+    auto issue_s = [&](int kk, int u) {
       A64_STAMP(g, kk, 3);  // S(kk) wants to issue
       wait_k(u);
       A64_STAMP(g, kk, 4);  // ... its K landed: issued
@@ -316,17 +375,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     mbar_wait(&bar_q[g], 0);  // Q rows of group g are in TMEM
     tc_fence_after();
-    if (n > 0) issue_s(0);
+    OwnWalk ow = own_start(g);
+    int u_next = n > 0 ? (kUnion ? own_next(ow, g) : seq_index(g, 0)) : -1;  // load index of own step k
+    if (n > 0) issue_s(0, u_next);
     for (int k = 0; k < n; ++k) {
-      // S(k+1) right after the softmax has loaded S(k), when its K has landed (a non-blocking
-      // probe: P.V(k) is not held up by a late K); otherwise after P.V(k). (Blocking here would
-      // also be safe: K(u) needs only the S MMAs of earlier loads, never a P.V.)
+      const int u = u_next;
+      const int u1 = k + 1 < n ? (kUnion ? own_next(ow, g) : seq_index(g, k + 1)) : -1;
+      u_next = u1;
+      // S(k+1) right after the softmax has loaded S(k) when its K has landed (a non-blocking
+      // probe: P.V(k) is not held up by a late K), otherwise after P.V(k). Step-major order
+      // could also block here (K(u) needs only the S MMAs of earlier loads); in union order
+      // a blocking wait is only safe within kKS positions of u: the stage then last held a
+      // position before u, which every chain releases without waiting on this one.
       mbar_wait(&bar_sfree[g], k & 1);
-      const int u1 = k + 1 < n ? seq_index(g, k + 1) : -1;
-      const bool early = u1 >= 0 && *reinterpret_cast<const volatile int*>(&k_issued) > u1 &&
-                         mbar_test_wait(&bar_kfull[u1 % kKS], (u1 / kKS) & 1);
-      if (early) issue_s(k + 1);
-      const int u = seq_index(g, k);
+      const bool early =
+          u1 >= 0 && ((kUnion && u1 - u < kKS) || (*reinterpret_cast<const volatile int*>(&k_issued) > u1 &&
+                                                   mbar_test_wait(&bar_kfull[u1 % kKS], (u1 / kKS) & 1)));
+      if (early) issue_s(k + 1, u1);
       mbar_wait(&bar_pfull[g], k & 1);  // P(k) of the group's 64 rows is in SMEM
       wait_v(u);
       A64_STAMP(g, k, 5);  // P(k) seen and V landed: P.V(k) issued
@@ -343,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bar_pvdone[g]);
       }
       __syncwarp();
-      if (!early && u1 >= 0) issue_s(k + 1);
+      if (!early && u1 >= 0) issue_s(k + 1, u1);
     }
     if (elect_one()) umma_commit(&bar_ofull[g]);
     __syncwarp();

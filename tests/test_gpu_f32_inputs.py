@@ -63,11 +63,22 @@ def test_f32_dense_attention_matches_oracle():
     assert np.abs(lse[0].cpu().numpy() - lser).max() <= 1e-2
 
 
-def test_async_mask_errors_visible_on_check():
+@pytest.mark.parametrize("impl", [0, 6])
+def test_async_mask_errors_visible_on_check(impl):
     """block_sparse_attention WITHOUT the synchronous check: a malformed mask (empty row /
     non-causal bit) is reported by us_check_device_errors through the workspace's sticky
-    error word, with the reference's message (attention.cpp:106-108, 127-129)."""
+    error word, with the reference's message (attention.cpp:106-108, 127-129) — by the
+    kernel the density gate picks (impl 0: attention.cu for this dense mask) and by
+    attention64.cu (impl 6, forced)."""
     api = us().api
+    assert api.lib().us_set_attention_impl(impl) == 0
+    try:
+        _async_mask_errors(api)
+    finally:
+        api.lib().us_set_attention_impl(0)
+
+
+def _async_mask_errors(api):
     rng = np.random.default_rng(5)
     Q = torch.from_numpy(rng.standard_normal((1, 2, 256, 64)).astype(np.float32)).to(torch.bfloat16).cuda()
     K = torch.from_numpy(rng.standard_normal((1, 2, 256, 64)).astype(np.float32)).to(torch.bfloat16).cuda()
