@@ -430,6 +430,7 @@ def main():
     launches_per_step = eng.launches()
     N = L // 64
     selected = int(eng.sel.counts.to(torch.int64).sum().item())
+    per_kv = eng.sel.counts.to(torch.int64).view(len(shard.batch), shard.H_kv, -1).sum(-1) * cfg.c_h  # [B, H_kv]
     # tile efficiency of attn_kernel: each M=128 tile (two 64-row query groups that
     # share a KV head) issues S / P.V for the UNION of its groups' selections
     tile_eff = None
@@ -624,9 +625,11 @@ def main():
     hbm, tf_burst, tf_sust, peak_src = peaks()
     flops_attn = selected * 4 * 64 * 64 * d
     dominant = max(stage_ms.items(), key=lambda kv: kv[1])[0]
-    # the kernel the device-side density gate runs (attn_common.cuh m64_wins, per call =
-    # per shard here): attention64.cu under 40 % of the causal block pairs selected
-    m64 = selected * 5 < causal * 2
+    # the kernel the device-side density gate runs (attn_common.cuh m64_wins, per (batch
+    # item, KV head)): attention64.cu under 55 % of the causal block pairs selected
+    kv_pairs = (len(heads) // shard.H_kv) * N * (N + 1) // 2
+    m64_frac = float(((per_kv * 20) < kv_pairs * 11).double().mean().item())
+    m64 = m64_frac >= 0.5
     if m64:
         # one M = 64 UMMA chain per query group: every issued row is a selected one, and an
         # M = 64 MMA occupies the tensor pipe for the cycles of M = 128 (B300_MICROARCH.md,
@@ -639,7 +642,8 @@ def main():
     if dominant == "attention":
         achieved = flops_attn / (stage_ms["attention"] * 1e-3) / 1e12
         roof = {"kernel": ("attn64_kernel (tcgen05 M=64 chains, block-sparse FA)" if m64 else
-                           "attn_kernel (tcgen05 block-sparse FA)"), "bound": "tensor", "achieved": achieved,
+                           "attn_kernel (tcgen05 block-sparse FA)"), "kv_heads_on_attn64": m64_frac,
+                "bound": "tensor", "achieved": achieved,
                 "peak": tf_sust, "unit": "TFLOP/s", "frac": achieved / tf_sust,
                 "algorithmic": "selected_blocks * 4 * S^2 * d (metrics.cpp:83-85)",
                 "issued_tflops": issued_attn / (stage_ms["attention"] * 1e-3) / 1e12 if issued_attn else None}

@@ -584,7 +584,7 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   if (mask && items && (impl == 6 || impl == 0)) {
     const long long entries = attention64_item_entries(g.B, g.H, g.H_kv, g.N);
     a.items = items;
-    a.row_counts = items + entries + 4;
+    a.row_counts = items + entries + 2 * g.B * g.H_kv;
     if (impl == 6) return launch_attention64(a, tK3, tV3, st);  // forced
     // automatic: the density is known on the device only; attention64's pre-pass counts the
     // selected pairs and each kernel's CTAs exit unless attn::m64_wins picks that kernel

@@ -167,7 +167,6 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
   __shared__ attn::Lists ls;
   __shared__ int kv_issued;  // union positions whose K/V load the producer has issued
 
-  if (a.sel_pairs && attn::m64_wins(a)) return;  // sparse enough for attention64.cu (launched before)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if US_ATTN_TRACE
   const bool us_traced = blockIdx.x == g_attn_trace_cta;
@@ -175,6 +174,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
   const int G = a.H / a.H_kv;
   const Groups gr = NT == 2 ? decode_item(a, blockIdx.x) : decode_pair(a, blockIdx.x);
   const int kvh = gr.h[0] / G;
+  if (a.sel_pairs && attn::m64_wins(a, gr.b, kvh)) return;  // sparse enough for attention64.cu (launched before)
   const int jmax = attn::last_block(a, gr);
 
   if (threadIdx.x == 0) {

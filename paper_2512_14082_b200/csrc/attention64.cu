@@ -135,7 +135,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto& n_own = ctl.n_own;
   uint32_t* const mrow = reinterpret_cast<uint32_t*>(smem + SL::kRowsOff);  // [4][W]: causal rows
 
-  if (a.sel_pairs && !attn::m64_wins(a)) return;  // the mask is dense enough for attn_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #if US_ATTN_TRACE
   const bool traced = int(blockIdx.x) == g_a64_trace_cta;
@@ -159,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gr = attn::decode_item(a, blockIdx.x);
     kvh = gr.h[0] / G;
   }
+  if (a.sel_pairs && !attn::m64_wins(a, gr.b, kvh)) return;  // dense enough for attn_kernel
   // mask row of chain g (its selected key blocks; read through L1 by the cursors below)
   auto row_of = [&](int g) {
     return a.mask + ((long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + gr.i[g]) * a.W;
@@ -578,7 +578,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Selected key blocks j <= i of every mask row (one warp per row, lanes over the row's
 // words), and their total over the heads (a.sel_pairs, the density gate's input).
 __global__ void __launch_bounds__(256) attn64_counts_kernel(AttnArgs a) {
-  __shared__ unsigned part[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long rows = (long long)a.B * a.planes * a.N;
   const long long r = (long long)blockIdx.x * 8 + warp;
@@ -593,15 +592,14 @@ __global__ void __launch_bounds__(256) attn64_counts_kernel(AttnArgs a) {
       n += __popc(word);
     }
     n = __reduce_add_sync(0xffffffffu, n);
-    if (lane == 0) a.row_counts[r] = int32_t(n);
-  }
-  if (a.sel_pairs) {
-    if (lane == 0) part[warp] = n;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t = 0;
-      for (int k = 0; k < 8; ++k) t += part[k];
-      if (t) atomicAdd(a.sel_pairs, t * (unsigned long long)a.heads_per_plane);
+    if (lane == 0) {
+      a.row_counts[r] = int32_t(n);
+      if (a.sel_pairs && n) {  // per (b, KV head) of each head the plane's row stands for
+        const int G = a.H / a.H_kv;
+        const int b = int(r / ((long long)a.planes * a.N)), pl = int((r / a.N) % a.planes);
+        for (int h = pl * a.heads_per_plane; h < (pl + 1) * a.heads_per_plane; ++h)
+          atomicAdd(&a.sel_pairs[b * a.H_kv + h / G], (unsigned long long)n);
+      }
     }
   }
 }
@@ -653,7 +651,8 @@ us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensor
     return s;
   long long items = attn::work_items(a);
   if (a.items) {
-    if (a.sel_pairs) US_CUDA_TRY(cudaMemsetAsync(a.sel_pairs, 0, sizeof(unsigned long long), st), "sel_pairs reset");
+    if (a.sel_pairs)
+      US_CUDA_TRY(cudaMemsetAsync(a.sel_pairs, 0, sizeof(unsigned long long) * a.B * a.H_kv, st), "sel_pairs reset");
     const long long rows = (long long)a.B * a.planes * a.N;
     attn64_counts_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(a);
     US_LAUNCH_CHECK("attn64_counts_kernel");
@@ -673,7 +672,7 @@ long long attention64_item_entries(int B, int H, int H_kv, int N) {
 }
 
 size_t attention64_ws_bytes(int B, int H, int H_kv, int N) {
-  return 4 * size_t(attention64_item_entries(B, H, H_kv, N)) + 16 + 4 * size_t(B) * H * N;
+  return 4 * size_t(attention64_item_entries(B, H, H_kv, N)) + 8 * size_t(B) * H_kv + 4 * size_t(B) * H * N;
 }
 
 us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st) {

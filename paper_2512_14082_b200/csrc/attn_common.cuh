@@ -94,12 +94,16 @@ inline long long work_items(const AttnArgs& a) {
 }
 
 // The automatic kernel choice for a mask (a.sel_pairs set): the M = 64 chains of
-// attention64.cu when under 40 % of the causal (i, j <= i) block pairs are selected, the
-// two-tile kernel otherwise. Measured crossover at C3 shapes (profiles/r02c/README.md):
-// attention64 0.92x the time of attn_kernel at 10.6 % selected, 0.98x at 32 %, 1.05x at 62 %.
-__device__ __forceinline__ bool m64_wins(const AttnArgs& a) {
-  const unsigned long long pairs = (unsigned long long)a.B * a.H * a.N * (a.N + 1) / 2;
-  return *a.sel_pairs * 5ull < pairs * 2ull;
+// attention64.cu when under 55 % of the causal (i, j <= i) block pairs are selected, the
+// two-tile kernel otherwise. Measured at C3 shapes, L = 64K (profiles/r02d/README.md):
+// attention64 takes 0.80x the time of attn_kernel at 10.6 % selected, 0.86x at 32 %, 0.95x
+// at 43 % and 50 %, 1.02x at 62 %, 1.07x at 81 %.
+// Decided per (batch item, KV head) — a unit every split of a call preserves (batch items,
+// the KV-head chunks of Engine.run_host), so a layer's output does not depend on how it
+// was partitioned.
+__device__ __forceinline__ bool m64_wins(const AttnArgs& a, int b, int kvh) {
+  const unsigned long long pairs = (unsigned long long)(a.H / a.H_kv) * a.N * (a.N + 1) / 2;
+  return a.sel_pairs[b * a.H_kv + kvh] * 20ull < pairs * 11ull;
 }
 
 __device__ __forceinline__ int last_block(const AttnArgs& a, const Groups& gr) {

@@ -148,9 +148,10 @@ struct AttnArgs {
   int32_t* items;       // attention64.cu: work-item table [B*H_kv][ceil(G*N/4)][4] of (h << 16 | i), -1 = none
                         // (nullable: the fixed decode_item order)
   int32_t* row_counts;   // attention64.cu: selected blocks j <= i per mask row [B][planes][N] (with a.items)
-  unsigned long long* sel_pairs;  // automatic choice (nullable = off): selected (i, j <= i) pairs of the mask,
-                                  // summed by attn64_items_kernel; both kernels are launched and each CTA
-                                  // exits unless attn::m64_wins(a) picks its kernel (attn_common.cuh)
+  unsigned long long* sel_pairs;  // automatic choice (nullable = off): selected (i, j <= i) pairs of the mask
+                                  // per (batch item, KV head) [B][H_kv], summed by attn64_counts_kernel; both
+                                  // kernels are launched and each CTA exits unless attn::m64_wins picks its
+                                  // kernel for its (b, KV head) (attn_common.cuh)
 };
 us_status launch_attention(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t st);
@@ -167,7 +168,7 @@ us_status launch_attention_tp(const AttnArgs& a, const CUtensorMap& tmQ, const C
 // tmK / tmV: 3-D rows-chunked maps (box 64 rows).
 us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st);
 // int32 entries of the attention64 work-item table (a.items) for these dims, and the bytes
-// of its workspace region: [item table][sel_pairs: 16 B][row_counts: B * H * N int32]
+// of its workspace region: [item table][sel_pairs: B * H_kv u64][row_counts: B * H * N int32]
 long long attention64_item_entries(int B, int H, int H_kv, int N);
 size_t attention64_ws_bytes(int B, int H, int H_kv, int N);
 
