@@ -216,6 +216,10 @@ inline void validate(const char* who, const us_params& p, bool need_compression 
 inline DeviceBuffer<uint8_t> workspace(const us_params& p) {
   return DeviceBuffer<uint8_t>(us_workspace_bytes(&p) + 256);
 }
+// the attention entry points' (much smaller) workspace
+inline DeviceBuffer<uint8_t> attention_workspace(const us_params& p) {
+  return DeviceBuffer<uint8_t>(us_attention_workspace_bytes(&p) + 256);
+}
 
 inline FlopBreakdown flops(const us_params& p) {
   uint64_t f[6];
@@ -348,7 +352,7 @@ inline AttentionOutput block_sparse_attention(const AttentionInputs& in, const B
   AttentionOutput out;
   out.O = DeviceBuffer<std::uint16_t>(size_t(in.B) * in.H * in.L * in.d_k);
   out.lse = DeviceBuffer<float>(size_t(in.B) * in.H * in.L);
-  auto ws = detail::workspace(p);
+  auto ws = detail::attention_workspace(p);
   detail::raise(us_sparse_attention(&p, in.Q, in.K, in.V, mask.bits.data(), mask.c_h, out.O.data(),
                                     out.lse.data(), ws.data(), ws.size(), in.stream));
   return out;
@@ -379,7 +383,7 @@ inline AttentionOutput dense_attention(const AttentionInputs& in, bool causal = 
   out.O = DeviceBuffer<std::uint16_t>(size_t(in.B) * in.H * in.L * in.d_k);
   out.lse = DeviceBuffer<float>(size_t(in.B) * in.H * in.L);
   DeviceBuffer<std::uint8_t> ws;  // f32 inputs: bf16 copies; d_k outside {64, 128}: padded copies
-  if (in.f32 || (in.d_k != 64 && in.d_k != 128)) ws = detail::workspace(p);
+  if (in.f32 || (in.d_k != 64 && in.d_k != 128)) ws = detail::attention_workspace(p);
   detail::raise(us_dense_attention(&p, in.Q, in.K, in.V, out.O.data(), out.lse.data(), ws.data(), ws.size(),
                                    in.stream));
   return out;

@@ -128,6 +128,14 @@ us_status us_check_params(const us_params* p, const char* who, int32_t need_comp
 /* Device workspace needed by any call below for these params. */
 size_t us_workspace_bytes(const us_params* p);
 
+/* The smaller workspace that suffices for us_sparse_attention / us_dense_attention
+ * (error header, bf16 copies of f32 inputs, the 64-granular mask for S > 64, the sparse
+ * kernel's work-item table, zero-padded d_k copies) — no proxy / selection buffers,
+ * which at the attention calls' c = 1 would scale with the uncompressed length. With
+ * at least this many bytes the attention calls report mask errors asynchronously
+ * (us_check_device_errors) and the density-gated sparse kernel runs. */
+size_t us_attention_workspace_bytes(const us_params* p);
+
 /* compress (compression.cpp:5-25), Mean pooling: Qc f32 [B][H/c_h][L/c_q][d_k],
  * Kc f32 [B][H/c_h][L/c_k][d_k] (K expanded to H heads first, as the reference). */
 us_status us_compress(const us_params* p, const void* Q, const void* K, float* Qc, float* Kc,

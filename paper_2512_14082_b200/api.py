@@ -96,6 +96,8 @@ def _bind(L: C.CDLL) -> C.CDLL:
     L.us_validate.argtypes = [C.POINTER(UsParams), C.c_char_p, C.c_size_t]
     L.us_workspace_bytes.restype = C.c_size_t
     L.us_workspace_bytes.argtypes = [C.POINTER(UsParams)]
+    L.us_attention_workspace_bytes.restype = C.c_size_t
+    L.us_attention_workspace_bytes.argtypes = [C.POINTER(UsParams)]
     vp = C.c_void_p
     L.us_compress.argtypes = [C.POINTER(UsParams), vp, vp, vp, vp, vp, C.c_size_t, vp]
     L.us_select.argtypes = [C.POINTER(UsParams), vp, vp, C.POINTER(UsSelection), vp, C.c_size_t, vp]
@@ -265,8 +267,10 @@ def _ws_key():
     return (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
 
 
-def workspace(p: UsParams) -> torch.Tensor:
-    need = lib().us_workspace_bytes(C.byref(p))
+def workspace(p: UsParams, attention_only: bool = False) -> torch.Tensor:
+    """The cached device workspace for a call: us_workspace_bytes, or the smaller
+    us_attention_workspace_bytes for block_sparse_attention / dense_attention."""
+    need = (lib().us_attention_workspace_bytes if attention_only else lib().us_workspace_bytes)(C.byref(p))
     key = _ws_key()
     cur = _ws_cache.get(key)
     if cur is None or cur.numel() < need:
@@ -430,8 +434,7 @@ def block_sparse_attention(Q, K, V, mask_bits: torch.Tensor, heads_per_plane: in
     O = torch.empty(Q.shape, dtype=torch.bfloat16, device=Q.device)
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
-    ws = workspace(p) if (validate_mask or Q.dtype == torch.float32 or S != 64 or Q.shape[-1] not in (64, 128)) \
-        else None
+    ws = workspace(p, attention_only=True)
     _raise(lib().us_sparse_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(mask_bits.contiguous()),
                                      heads_per_plane, _ptr(O), _ptr(lse), _ptr(ws),
                                      ws.numel() if ws is not None else 0, _stream()))
@@ -467,7 +470,7 @@ def dense_attention(Q, K, V, S: int = 64, with_lse: bool = True, causal: bool = 
     B, H, L, _ = _bhld(Q)
     lse = torch.empty((B, H, L), dtype=torch.float32, device=Q.device) if with_lse else None
     # f32 inputs: bf16 copies in the workspace; d_k outside {64, 128}: zero-padded copies
-    ws = workspace(p) if (Q.dtype == torch.float32 or Q.shape[-1] not in (64, 128)) else None
+    ws = workspace(p, attention_only=True) if (Q.dtype == torch.float32 or Q.shape[-1] not in (64, 128)) else None
     _raise(lib().us_dense_attention(C.byref(p), _ptr(Q), _ptr(K), _ptr(V), _ptr(O), _ptr(lse), _ptr(ws),
                                     ws.numel() if ws is not None else 0, _stream()))
     return O, lse

@@ -180,7 +180,11 @@ size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 // scores_region: the [B][planes][N][N] f32 block-score tensor, needed only by the
 // competitor proxies and exact_block_mass; the UniSparse path fuses the block
 // scores into the selection (select_fused_kernel) and never materialises them.
-Ws layout(const us_params& p, bool scores_region = false) {
+// attn_only: the attention entry points (block_sparse_attention, dense_attention) need
+// only the error header, the bf16 copies of f32 inputs, the 64-granular mask and the
+// attention64 item table — not the proxy / selection buffers, which at c = 1 (the
+// attention-only params) would scale with the uncompressed length.
+Ws layout(const us_params& p, bool scores_region = false, bool attn_only = false) {
   Geo g(p);
   Ws w{};
   size_t o = 0;
@@ -196,6 +200,7 @@ Ws layout(const us_params& p, bool scores_region = false) {
   w.absmax_q = take(4 * qplanes);
   w.absmax_k = take(4 * kplanes);
   w.header_bytes = o;
+  if (!attn_only) {
   w.exp_q = take(4 * qplanes * g.Lq);  // one scale exponent per composite query row
   w.exp_k = take(4 * kplanes);
   const size_t rows = qplanes * g.N;
@@ -216,6 +221,7 @@ Ws layout(const us_params& p, bool scores_region = false) {
   w.tmax = take(4 * qplanes * T * g.Lq);
   w.scores = scores_region ? take(4 * rows * g.N) : 0;
   w.mask = take(4 * rows * g.W);
+  }
   // f32 inputs: bf16 copies of Q, K, V for the attention kernels
   w.conv = p.dtype == US_DTYPE_F32 ? take(2 * (size_t(g.B) * g.H + 2 * size_t(g.B) * g.H_kv) * g.L * g.D) : 0;
   // S > 64: the 64-granular copy of the block mask the attention kernels walk (one plane per head)
@@ -232,8 +238,9 @@ T* at(void* ws, size_t off) {
   return reinterpret_cast<T*>(static_cast<uint8_t*>(ws) + off);
 }
 
-us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, bool scores_region = false) {
-  const size_t need = layout(p, scores_region).total;
+us_status need_ws(const us_params& p, void* ws, size_t bytes, const char* who, bool scores_region = false,
+                  bool attn_only = false) {
+  const size_t need = layout(p, scores_region, attn_only).total;
   if (!ws || bytes < need) {
     set_error(std::string(who) + ": workspace of " + std::to_string(need) + " bytes required");
     return US_ERR_WORKSPACE;
@@ -271,7 +278,9 @@ us_params padded_params(const us_params& p) {
   q.d_k = padded_dk(p.d_k);
   return q;
 }
-size_t padded_ws_bytes(const us_params& p) { return al(layout(padded_params(p)).total) + pad_layout(p).total; }
+size_t padded_ws_bytes(const us_params& p, bool attn_only = false) {
+  return al(layout(padded_params(p), false, attn_only).total) + pad_layout(p).total;
+}
 
 struct PadStage {
   us_params pp;        // the same call at the padded width
@@ -603,17 +612,17 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
 us_status run_attention(const us_params& p, const void* Q, const void* K, const void* V,
                         const uint32_t* mask, int hpp, void* O, float* lse, cudaStream_t st,
                         uint32_t* err = nullptr, int32_t* first_bad = nullptr, void* ws = nullptr,
-                        bool ws_ok = false) {
+                        bool ws_ok = false, bool attn_only = false) {
   Geo g(p);
   us_params q = p;
-  int32_t* items = (ws && ws_ok) ? at<int32_t>(ws, layout(p).items) : nullptr;
+  int32_t* items = (ws && ws_ok) ? at<int32_t>(ws, layout(p, false, attn_only).items) : nullptr;
   if (p.S == kGpuBlock && p.dtype == US_DTYPE_BF16)
     return run_attention_core(q, Q, K, V, mask, hpp, O, lse, st, err, first_bad, items);
   if (!ws && (p.dtype == US_DTYPE_F32 || (mask && p.S != kGpuBlock))) {
-    set_error("attention: f32 inputs / S != 64 need the workspace (us_workspace_bytes)");
+    set_error("attention: f32 inputs / S != 64 need the workspace (us_attention_workspace_bytes)");
     return US_ERR_WORKSPACE;
   }
-  Ws w = layout(p);
+  Ws w = layout(p, false, attn_only);
   us_status s;
   if (p.S != kGpuBlock) {
     // S = 64 m: the kernels walk 64-row / 64-key sub-blocks of the selected blocks
@@ -755,6 +764,12 @@ size_t us_workspace_bytes(const us_params* p) {
   if (!p || !check(*p, false).errors.empty()) return 0;
   if (needs_pad(*p) && p->d_k <= 128) return padded_ws_bytes(*p);
   return layout(*p).total;
+}
+
+size_t us_attention_workspace_bytes(const us_params* p) {
+  if (!p || !check(*p, false).errors.empty()) return 0;
+  if (needs_pad(*p) && p->d_k <= 128) return padded_ws_bytes(*p, true);
+  return layout(*p, false, true).total;
 }
 
 us_status us_compress(const us_params* p, const void* Q, const void* K, float* Qc, float* Kc,
@@ -1096,7 +1111,9 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (needs_pad(*p)) {
     PadStage ps;
-    if ((s = pad_begin(*p, workspace, workspace_bytes, "block_sparse_attention", ps)) != US_OK) return s;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "block_sparse_attention", ps,
+                       layout(padded_params(*p), false, true).total)) != US_OK)
+      return s;
     if ((s = pad_inputs(*p, ps, Q, K, V, st)) != US_OK) return s;
     {
       ScaleDk scale(p->d_k);
@@ -1109,8 +1126,8 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
     return US_OK;
   }
   if (p->flags & US_FLAG_SYNC_CHECK) {
-    if ((s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK) return s;
-    Ws w = layout(*p);
+    if ((s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention", false, true)) != US_OK) return s;
+    Ws w = layout(*p, false, true);
     US_CUDA_TRY(cudaMemsetAsync(workspace, 0, 4, st), "workspace clear");
     US_CUDA_TRY(cudaMemsetAsync(at<uint8_t>(workspace, w.first_bad), 0x7F, 4, st), "workspace clear");
     if ((s = launch_mask_check(mask_bits, g.B * (g.H / heads_per_plane) * g.N, g.N, g.W,
@@ -1119,21 +1136,21 @@ us_status us_sparse_attention(const us_params* p, const void* Q, const void* K, 
     if ((s = sync_check(*p, workspace, st, "block_sparse_attention")) != US_OK) return s;
   }
   if ((p->dtype == US_DTYPE_F32 || p->S != kGpuBlock) &&
-      (s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention")) != US_OK)
+      (s = need_ws(*p, workspace, workspace_bytes, "block_sparse_attention", false, true)) != US_OK)
     return s;
   uint32_t* err = nullptr;
   int32_t* first_bad = nullptr;
-  if (workspace && workspace_bytes >= layout(*p).total) {
+  if (workspace && workspace_bytes >= layout(*p, false, true).total) {
     // asynchronous data-error report (us_check_device_errors): the kernel ORs 4 (a
     // non-causal bit) or 8 (an empty row) into the sticky error word and records the
     // first offending row, as the reference throws (attention.cpp:106-108, 127-129)
-    Ws w = layout(*p);
+    Ws w = layout(*p, false, true);
     err = at<uint32_t>(workspace, w.err);
     first_bad = at<int32_t>(workspace, w.first_bad);
     US_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7F, 4, st), "workspace clear");
   }
   if ((s = run_attention(*p, Q, K, V, mask_bits, heads_per_plane, O, lse, st, err, first_bad, workspace,
-                         workspace && workspace_bytes >= layout(*p).total)) != US_OK)
+                         workspace && workspace_bytes >= layout(*p, false, true).total, true)) != US_OK)
     return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "block_sparse_attention");
   return US_OK;
@@ -1185,7 +1202,9 @@ us_status us_dense_attention(const us_params* p, const void* Q, const void* K, c
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (needs_pad(*p)) {
     PadStage ps;
-    if ((s = pad_begin(*p, workspace, workspace_bytes, "dense_attention", ps)) != US_OK) return s;
+    if ((s = pad_begin(*p, workspace, workspace_bytes, "dense_attention", ps,
+                       layout(padded_params(*p), false, true).total)) != US_OK)
+      return s;
     if ((s = pad_inputs(*p, ps, Q, K, V, st)) != US_OK) return s;
     {
       ScaleDk scale(p->d_k);
@@ -1196,8 +1215,9 @@ us_status us_dense_attention(const us_params* p, const void* Q, const void* K, c
     Geo g(*p);
     return unpad_rows(ps.base + ps.w.o, O, size_t(g.B) * g.H * g.L, g.D, ps.pp.d_k, 2, st);
   }
-  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "dense_attention")) != US_OK) return s;
-  if ((s = run_attention(*p, Q, K, V, nullptr, 1, O, lse, st, nullptr, nullptr, workspace)) != US_OK) return s;
+  if (p->dtype == US_DTYPE_F32 && (s = need_ws(*p, workspace, workspace_bytes, "dense_attention", false, true)) != US_OK) return s;
+  if ((s = run_attention(*p, Q, K, V, nullptr, 1, O, lse, st, nullptr, nullptr, workspace, false, true)) != US_OK)
+    return s;
   if (p->flags & US_FLAG_SYNC_CHECK) US_CUDA_TRY(cudaStreamSynchronize(st), "dense_attention");
   return US_OK;
 }

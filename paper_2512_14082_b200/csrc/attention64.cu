@@ -91,7 +91,6 @@ struct A64Smem {
     uint32_t tmem_base;
     int k_issued, v_issued;  // loads of the sequence whose K / V the producer has issued
     int n_own[4];            // own steps (selected blocks j <= i) of each chain
-    int n_union;             // union positions (blocks any chain selected)
   };
   static constexpr int kCtlOff = kRingBytes + 4 * kPBytes;
   static constexpr int kRowsOff = kCtlOff + (int(sizeof(Ctl)) + 15) / 16 * 16;
@@ -185,39 +184,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&ctl.tmem_base, 512);
-  if (warp == 0) {
-    // the causal rows of the four chains -> shared memory, own steps of each chain (their
-    // popcounts) and the asynchronous data-error report (the reference throws,
-    // attention.cpp:106-108, 127-129): a non-causal bit anywhere in the row, or an empty
-    // causal prefix
-    for (int g = 0; g < 4; ++g) {
-      unsigned c = 0, bad = 0;
-      const uint32_t* src = row_of(g);
-      const int ig = gr.i[g];
-      for (int w = lane; w < a.W; w += 32) {
-        const uint32_t word = gr.en[g] ? src[w] : 0u;
-        const int lo = w << 5;
-        const uint32_t keep = lo > ig ? 0u : (ig - lo >= 31 ? ~0u : (2u << (ig - lo)) - 1u);
-        bad |= word & ~keep;
-        c += __popc(word & keep);
-        mrow[g * a.W + w] = word & keep;
-      }
-      c = __reduce_add_sync(0xffffffffu, c);
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (lane == 0) {
-        n_own[g] = int(c);
-        if (a.err && gr.en[g] && (bad || c == 0)) {
-          atomicOr(a.err, bad ? 4u : 8u);
-          atomicMin(a.first_bad, int32_t((src - a.mask) / a.W));
-        }
+  // softmax warps: this thread's half of its Q row, prefetched before the prologue barrier
+  // (written to TMEM after it)
+  constexpr int kQv = D / 16;  // uint4 per half row
+  uint4 qpre[kQv];
+  if (warp >= 4 && warp < 20) {
+    const int g = (warp - 4) >> 2, q = warp & 3, half = lane >> 4, r = 16 * q + (lane & 15);
+    const uint4* src = reinterpret_cast<const uint4*>(
+        a.Q + ((long long)(gr.b * a.H + gr.h[g]) * a.L + (long long)gr.i[g] * kBS + r) * D) + half * kQv;
+#pragma unroll
+    for (int u = 0; u < kQv; ++u) qpre[u] = gr.en[g] ? __ldg(src + u) : make_uint4(0, 0, 0, 0);
+  }
+  if (warp < 4) {
+    // warp g: chain g's causal row -> shared memory, its own steps (popcount) and the
+    // asynchronous data-error report (the reference throws, attention.cpp:106-108,
+    // 127-129): a non-causal bit anywhere in the row, or an empty causal prefix
+    const int g = warp;
+    unsigned c = 0, bad = 0;
+    const uint32_t* src = row_of(g);
+    const int ig = gr.i[g];
+    for (int w = lane; w < a.W; w += 32) {
+      const uint32_t word = gr.en[g] ? src[w] : 0u;
+      const int lo = w << 5;
+      const uint32_t keep = lo > ig ? 0u : (ig - lo >= 31 ? ~0u : (2u << (ig - lo)) - 1u);
+      bad |= word & ~keep;
+      c += __popc(word & keep);
+      mrow[g * a.W + w] = word & keep;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      n_own[g] = int(c);
+      if (a.err && gr.en[g] && (bad || c == 0)) {
+        atomicOr(a.err, bad ? 4u : 8u);
+        atomicMin(a.first_bad, int32_t((src - a.mask) / a.W));
       }
     }
-    __syncwarp();
-    unsigned nu = 0;
-    for (int w = lane; w < a.W; w += 32)
-      nu += __popc(mrow[w] | mrow[a.W + w] | mrow[2 * a.W + w] | mrow[3 * a.W + w]);
-    nu = __reduce_add_sync(0xffffffffu, nu);
-    if (lane == 0) ctl.n_union = int(nu);
   }
   tc_fence_before();
   __syncthreads();
@@ -230,7 +232,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     return min(k, n0) + min(k, n1) + min(k, n2) + min(k, n3) + (g > 0 && n0 > k) + (g > 1 && n1 > k) +
            (g > 2 && n2 > k);
   };
-  const int T = kUnion ? ctl.n_union : n0 + n1 + n2 + n3;  // loads of the sequence
+  auto union_count = [&]() {  // (warp-wide) blocks any chain selected
+    unsigned nu = 0;
+    for (int w = lane; w < a.W; w += 32)
+      nu += __popc(mrow[w] | mrow[a.W + w] | mrow[2 * a.W + w] | mrow[3 * a.W + w]);
+    return int(__reduce_add_sync(0xffffffffu, nu));
+  };
   auto union_word = [&](int w) {
     return mrow[w] | mrow[a.W + w] | mrow[2 * a.W + w] | mrow[3 * a.W + w];
   };
@@ -259,22 +266,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 || warp >= 21) {
     // ------------------------------------------------------------ TMA producers
-    // The load sequence is step-major: round k loads the k-th own block of chain 0, 1, 2, 3
-    // (seq_index). The chains of a CTA have near-equal lengths (the sorted work items) and
-    // advance together, so the ring windows hold the next steps of every chain; a
-    // union-ordered sequence (ascending j) lets a chain whose blocks sit early in j fill the
-    // ring while the others starve. A block two chains selected is loaded twice.
-    // K and V are two sequences (a K tile is only held until its S retires, so K runs ahead):
-    // K(u) once K stage u % kKS is free, V(u) once V stage u % kVS is. One warp issues only
-    // ~20-29 B/clk of bulk / tensor copies however deep its ring (tools/tma_probe.cu: the
-    // copies of one issuing warp proceed one at a time; four issuing warps reach the
-    // ~70 B/clk/SM L2 -> SMEM ceiling), so each sequence is dealt round-robin to two warps
-    // (K: warps 0, 21; V: warps 22, 23). Arming a load (stage free, expect_tx, the issued
-    // count) stays in sequence order; the copies run in parallel.
+    // The load sequence (US_A64_UNION): union order — ascending j over the four chains'
+    // selected blocks, a block several chains selected loaded once (0.74 / 0.56 loads per
+    // own step at C3 gain 9 / 8), the producer releasing each position for the chains that
+    // skip it — or step-major (round k = the k-th block of chain 0, 1, 2, 3; every load
+    // belongs to one chain). K and V are two sequences (a K tile is only held until its S
+    // retires, so K runs ahead): K(u) once K stage u % kKS is free, V(u) once V stage
+    // u % kVS is. One warp issues only ~20-29 B/clk of bulk / tensor copies however deep
+    // its ring (tools/tma_probe.cu: the copies of one issuing warp proceed one at a time;
+    // four issuing warps reach the ~70 B/clk/SM L2 -> SMEM ceiling), so each sequence is
+    // dealt round-robin to two warps (K: warps 0, 21; V: warps 22, 23). Arming a load
+    // (stage free, expect_tx, skip releases, the issued count) stays in sequence order;
+    // the copies run in parallel.
     const int pw = warp == 0 ? 0 : warp - 20;  // 0 .. kKProd - 1: K producers; the rest V
     constexpr int kKProd = US_A64_KPROD;
     const bool is_v = pw >= kKProd;
     const int np = is_v ? 4 - kKProd : kKProd, me = is_v ? pw - kKProd : pw;
+    const int total = kUnion ? union_count() : n0 + n1 + n2 + n3;  // loads of the sequence
     if (elect_one()) {
       if (pw == 0) {
         tma_prefetch_desc(&tmK);
@@ -282,7 +290,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint64_t pol_kv = policy_evict_last();
       const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
-      const int total = T;
       const int nmax = max(max(n0, n1), max(n2, n3));
       const CUtensorMap* tm = is_v ? &tmV : &tmK;
       const int nst = is_v ? kVS : kKS;
@@ -426,15 +433,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = a.scale_log2;
     float m_used = -INFINITY, l = 0.f;  // l: this thread's half of the row sum
     {
-      // this half of the Q row -> TMEM (A operand of S = Q K^T, 2 bf16 per column)
-      const uint4* src = reinterpret_cast<const uint4*>(
-          a.Q + ((long long)(gr.b * a.H + hg) * a.L + (long long)ig * kBS + r) * D);
+      // this half of the Q row (prefetched) -> TMEM (A operand of S = Q K^T, 2 bf16 per column)
 #pragma unroll
       for (int c0 = 0; c0 < D / 4; c0 += 16) {
         uint32_t w16[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint4 v = en ? __ldg(src + (half * (D / 4) + c0) / 4 + u) : make_uint4(0, 0, 0, 0);
+          const uint4 v = qpre[c0 / 4 + u];
           w16[4 * u] = v.x;
           w16[4 * u + 1] = v.y;
           w16[4 * u + 2] = v.z;

@@ -79,6 +79,26 @@ def test_padded_dk_workspace_bytes(lib):
     assert ws32 >= ws64 + padded
 
 
+def test_attention_workspace_is_small_at_c3(lib):
+    """The attention entry points' workspace (us_attention_workspace_bytes) holds only the
+    error header and the sparse kernel's work-item table at C3 (32 / 8 heads, L = 128K,
+    d = 128, c = 1): megabytes — the full pipeline layout at c = 1 would size the proxy
+    buffers for the uncompressed length (hundreds of GB)."""
+    from paper_2512_14082_b200.api import UsParams
+    for f in (lib.us_workspace_bytes, lib.us_attention_workspace_bytes):
+        f.argtypes = [C.POINTER(UsParams)]
+        f.restype = C.c_size_t
+    p = UsParams(1, 32, 8, 131072, 128, 64, 1, 1, 1, 0, 0, 0, 0.95, 0, 0, 0)
+    N = 131072 // 64
+    attn = lib.us_attention_workspace_bytes(C.byref(p))
+    items = 4 * 8 * ((4 * N + 3) // 4) * 4 + 8 * 8 + 4 * 32 * N  # item table, sel_pairs, row counts
+    assert items <= attn < items + 64 * 1024, attn
+    assert lib.us_workspace_bytes(C.byref(p)) > 100 * attn
+    p.dtype = 1  # f32 inputs: + bf16 copies of Q, K, V
+    conv = 2 * (32 + 2 * 8) * 131072 * 128
+    assert lib.us_attention_workspace_bytes(C.byref(p)) >= conv + items
+
+
 def test_cpp_wrapper_cpu():
     if not os.path.exists(WRAPPER):
         from paper_2512_14082_b200 import build
