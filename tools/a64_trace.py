@@ -56,7 +56,7 @@ for g in range(4):
           f"S(k+1) issued after P.V(k) {(e[4][1:] > e[5][:-1]).mean()*100:.0f}%")
     summ.append(period.mean())
     if g < 2:
-        print("   k    u |  S req  S iss  Kload(u) | sm want  S seen  exps  P hand | PV iss")
+        print("   k    t |  S req  S iss  Kload(t) | sm want  S seen  exps  P hand | PV iss")
         for k in range(min(n, 24)):
             print(f"{k:4d} {pos[k]:4d} | {e[3][k]:6d} {e[4][k]:6d} {load[k]:7d} | {e[0][k]:7d} {e[1][k]:7d} "
                   f"{e[2][k]:6d} {e[6][k]:6d} | {e[5][k]:6d}")
