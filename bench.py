@@ -518,6 +518,23 @@ def main():
     e2e_ms = max_over_ranks(e2.elapsed_time(e3) / args.steps)
     e2e_exact = e2e_exact and bool(torch.equal(Oh.to(eng.O.device), O_ref))
     del O_ref
+    # (c) the copy floor: the same H2D and D2H bytes on two streams with no compute (this
+    # box's PCIe link does not run both directions at full rate at once)
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    e2.record(stream)
+    for _ in range(3):
+        with torch.cuda.stream(s_in):
+            Q.copy_(Qh, non_blocking=True)
+            K.copy_(Kh, non_blocking=True)
+            V.copy_(Vh, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            Oh.copy_(eng.O, non_blocking=True)
+        stream.wait_stream(s_in)
+        stream.wait_stream(s_out)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    copy_floor_ms = e2.elapsed_time(e3) / 3
     def sum_over_ranks(x: float) -> float:
         if not dist:
             return x
@@ -713,6 +730,7 @@ def main():
                             f"{args.e2e_chunks} KV-head chunks on 4 streams (copy-in, 2 compute with 2 chunk workspaces, copy-out), "
                             f"consecutive steps overlapped per chunk",
                     "serial_ms": e2e_serial_ms,
+                    "copy_floor_ms": copy_floor_ms,
                     "output_equals_device_path": e2e_exact},
                gpu_launches=launches_per_step * args.steps,
                roofline=roof, cpu_baseline=cpu,
