@@ -352,6 +352,34 @@ def test_automatic_choice_follows_the_density_gate(density, H, H_kv, d):
             assert torch.equal(out[0][1][b, hs], out[want][1][b, hs]), (b, g, frac, want)
 
 
+@pytest.mark.parametrize("N,H,H_kv,d", [(33, 8, 2, 128), (45, 6, 6, 64), (45, 7, 1, 128)])
+def test_attention64_odd_block_counts(N, H, H_kv, d):
+    """attention64.cu (forced, and through the automatic gate) at block counts that end
+    mid-word of the 32-bit mask rows, with GQA, MHA and G = 7 (a CTA's four chains drawn
+    from different heads and query blocks by the sorted item table): equal to the fp64
+    oracle within the bf16 tolerance."""
+    rng = np.random.default_rng(N * 10 + H)
+    B, L = 2, N * 64
+    Q, K, V = _rand_qkv(rng, B, H, H_kv, L, d)
+    mask = rng.random((B, H, N, N)) < 0.25
+    mask &= np.tril(np.ones((N, N), bool))
+    mask[..., np.arange(N), np.arange(N)] = True
+    bits = torch.from_numpy(_bits_from_mask(mask)).cuda()
+    try:
+        for impl in (6, 0):
+            _set_impl(impl)
+            Og, lseg = us().block_sparse_attention(to_dev_bf16(Q), to_dev_bf16(K), to_dev_bf16(V), bits)
+            Og = Og.float().cpu().numpy()
+            lseg = lseg.cpu().numpy()
+            for b in range(B):
+                Or, lser = O.block_sparse_attention(Q[b], K[b], V[b], mask[b], 64)
+                assert np.abs(Og[b] - Or).max() <= ATOL, (impl, b)
+                assert np.linalg.norm(Og[b] - Or) / np.linalg.norm(Or) <= RTOL_FRO, (impl, b)
+                assert np.abs(lseg[b] - lser).max() <= 1e-3, (impl, b)
+    finally:
+        _set_impl(0)
+
+
 def test_product_library_has_no_calibration_variants():
     """The product library runs attention.cu only: the calibration variants (2-5) and the
     probes are absent from libunisparse_b200.so (they live in the calibration build)."""
