@@ -590,19 +590,21 @@ us_status run_attention_core(const us_params& p, const void* Q, const void* K, c
   a.one_tile = impl == 3 ? 1 : 0;
   if (impl == 5) return launch_attention_tp(a, tQ, tK3, tV3, st);
 #endif
+  CUtensorMap tQa;  // attention64.cu: one TMA per 64 Q rows (all d-chunks)
+  if (mask && (s = make_tmap_rows_chunked(&tQa, Q, uint64_t(g.B) * g.H * g.L, g.D, 64)) != US_OK) return s;
   if (mask && items && (impl == 6 || impl == 0)) {
     const long long entries = attention64_item_entries(g.B, g.H, g.H_kv, g.N);
     a.items = items;
     a.row_counts = items + entries + 2 * g.B * g.H_kv;
-    if (impl == 6) return launch_attention64(a, tK3, tV3, st);  // forced
+    if (impl == 6) return launch_attention64(a, tQa, tK3, tV3, st);  // forced
     // automatic: the density is known on the device only; attention64's pre-pass counts the
     // selected pairs and each kernel's CTAs exit unless attn::m64_wins picks that kernel
     a.sel_pairs = reinterpret_cast<unsigned long long*>(items + entries);
-    if ((s = launch_attention64(a, tK3, tV3, st)) != US_OK) return s;
+    if ((s = launch_attention64(a, tQa, tK3, tV3, st)) != US_OK) return s;
     a.items = nullptr;
     a.row_counts = nullptr;
   } else if (mask && impl == 6) {
-    return launch_attention64(a, tK3, tV3, st);  // forced, no workspace: the fixed decode order
+    return launch_attention64(a, tQa, tK3, tV3, st);  // forced, no workspace: the fixed decode order
   }
   return launch_attention(a, tQ, tK3, tV3, st);
 }

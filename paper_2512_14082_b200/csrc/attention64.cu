@@ -27,6 +27,10 @@
 //   copies, as one issuing warp caps at ~20-29 B/clk (tools/tma_probe.cu).
 // * The four chains' causal mask rows live in shared memory (the producers' walk); all
 //   shared memory is dynamic (the rows' size follows W).
+// * Q arrives by TMA too: each producer copies one group's 64 rows into a V stage that is
+//   idle at CTA start, and the softmax warps move it to TMEM, after which the V stream
+//   starts. The softmax warps' own 16-B row loads took ~7 k cycles at CTA start and held
+//   the first K copy behind them (a CTA's fixed cost: ~25 k -> ~20 k cycles).
 //
 // Warps (768 threads): 0 row loader + K producer, 21 K producer, 22-23 V producers, 1-3 and 20
 // MMA issuers of groups 0-3 (warp 1 owns TMEM), 4-19 softmax (warp 4 + 4 g + q: group g, lane
@@ -88,6 +92,8 @@ struct A64Smem {
   struct Ctl {
     uint64_t bar_q[4], bar_kfull[kKS], bar_kempty[kKS], bar_vfull[kVS], bar_vempty[kVS], bar_sfull[4], bar_sfree[4],
         bar_pfull[4], bar_pvdone[4], bar_ofull[4];
+    uint64_t bar_qfull[4];  // group g's Q rows have landed in V stage g (TMA)
+    uint64_t bar_qfree;     // the 16 softmax warps have read their Q rows: V stages 0-3 are free
     uint32_t tmem_base;
     int k_issued, v_issued;  // loads of the sequence whose K / V the producer has issued
     int n_own[4];            // own steps (selected blocks j <= i) of each chain
@@ -108,8 +114,8 @@ __device__ __forceinline__ int issuer_group(int warp) { return warp == 20 ? 3 : 
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
-    attn64_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                  const AttnArgs a) {
+    attn64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using SL = A64Smem<D>;
   constexpr int kKS = SL::kKS, kVS = SL::kVS;
   constexpr bool kUnion = US_A64_UNION != 0;
@@ -158,6 +164,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     kvh = gr.h[0] / G;
   }
   if (a.sel_pairs && !attn::m64_wins(a, gr.b, kvh)) return;  // dense enough for attn_kernel
+  if (threadIdx.x == 0) {
+    A64_STAMP(4, 4090, 0);  // (trace) CTA lifecycle: entry
+    // the tensor-map descriptors, well before the first copy needs them
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+  }
   // mask row of chain g (its selected key blocks; read through L1 by the cursors below)
   auto row_of = [&](int g) {
     return a.mask + ((long long)(gr.b * a.planes + gr.h[g] / a.heads_per_plane) * a.N + gr.i[g]) * a.W;
@@ -172,6 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_pvdone[g], 1);
       mbar_init(&bar_ofull[g], 1);
     }
+    for (int g = 0; g < 4; ++g) mbar_init(&ctl.bar_qfull[g], 1);
+    mbar_init(&ctl.bar_qfree, 16);
     for (int s = 0; s < kKS; ++s) {
       mbar_init(&bar_kfull[s], 1);
       mbar_init(&bar_kempty[s], kEmptyCount);
@@ -184,17 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&ctl.tmem_base, 512);
-  // softmax warps: this thread's half of its Q row, prefetched before the prologue barrier
-  // (written to TMEM after it)
-  constexpr int kQv = D / 16;  // uint4 per half row
-  uint4 qpre[kQv];
-  if (warp >= 4 && warp < 20) {
-    const int g = (warp - 4) >> 2, q = warp & 3, half = lane >> 4, r = 16 * q + (lane & 15);
-    const uint4* src = reinterpret_cast<const uint4*>(
-        a.Q + ((long long)(gr.b * a.H + gr.h[g]) * a.L + (long long)gr.i[g] * kBS + r) * D) + half * kQv;
-#pragma unroll
-    for (int u = 0; u < kQv; ++u) qpre[u] = gr.en[g] ? __ldg(src + u) : make_uint4(0, 0, 0, 0);
-  }
+  if (threadIdx.x == 32) A64_STAMP(4, 4091, 1);  // (trace) TMEM allocated
   if (warp < 4) {
     // warp g: chain g's causal row -> shared memory, its own steps (popcount) and the
     // asynchronous data-error report (the reference throws, attention.cpp:106-108,
@@ -220,10 +225,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         atomicMin(a.first_bad, int32_t((src - a.mask) / a.W));
       }
     }
+    if (threadIdx.x == 0) A64_STAMP(4, 4091, 0);  // (trace) row 0 in shared memory
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) A64_STAMP(4, 4090, 1);  // (trace) prologue barrier passed
   const uint32_t tmem = ctl.tmem_base;
   const int n0 = n_own[0], n1 = n_own[1], n2 = n_own[2], n3 = n_own[3];
   // index of chain g's own step k in the load sequence (round k: chains 0-3 in order, a
@@ -283,11 +290,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool is_v = pw >= kKProd;
     const int np = is_v ? 4 - kKProd : kKProd, me = is_v ? pw - kKProd : pw;
     const int total = kUnion ? union_count() : n0 + n1 + n2 + n3;  // loads of the sequence
+    if (threadIdx.x == 0) A64_STAMP(4, 4091, 3);  // (trace) producer 0: union counted
     if (elect_one()) {
-      if (pw == 0) {
-        tma_prefetch_desc(&tmK);
-        tma_prefetch_desc(&tmV);
+      // first, producer pw's copy of group pw's 64 Q rows (16 KB at d = 128) into V stage pw,
+      // idle until the first V loads: four producers issue them at once (one issuing warp's
+      // copies proceed one at a time), fully coalesced — the softmax warps' own 16-B row
+      // loads of Q took ~7 k cycles at CTA start and held the first K copy behind them
+      {
+        const int gq = pw;
+        if (gr.en[gq]) {
+          mbar_arrive_expect_tx(&ctl.bar_qfull[gq], SL::kKVBytes);
+          tma_load_3d_hint(smem + (kKS + gq) * SL::kKVBytes, &tmQ, &ctl.bar_qfull[gq], 0,
+                           (gr.b * a.H + gr.h[gq]) * a.L + gr.i[gq] * kBS, 0, policy_evict_first());
+        } else {
+          mbar_arrive(&ctl.bar_qfull[gq]);
+        }
       }
+      if (is_v) mbar_wait(&ctl.bar_qfree, 0);  // V stages 0-3 hold Q until the softmax warps read it
       const uint64_t pol_kv = policy_evict_last();
       const int kvrow0 = (gr.b * a.H_kv + kvh) * a.L;
       const int nmax = max(max(n0, n1), max(n2, n3));
@@ -433,13 +452,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = a.scale_log2;
     float m_used = -INFINITY, l = 0.f;  // l: this thread's half of the row sum
     {
-      // this half of the Q row (prefetched) -> TMEM (A operand of S = Q K^T, 2 bf16 per column)
+      // this half of the Q row: from V stage g (the producers' SWIZZLE_128B copy: d-chunk c of
+      // row r at c * 8 KB + r * 128, 16-B unit u at (u ^ (r & 7)) * 16) -> TMEM (A operand of
+      // S = Q K^T, 2 bf16 per column)
+      constexpr int kQv = D / 16;  // 16-B units per half row
+      uint4 qv[kQv];
+      mbar_wait(&ctl.bar_qfull[g], 0);
+      const uint8_t* qs = smem + (kKS + g) * SL::kKVBytes;
+#pragma unroll
+      for (int u = 0; u < kQv; ++u) {
+        const int U = half * kQv + u, c = U >> 3, cu = U & 7;
+        qv[u] = en ? *reinterpret_cast<const uint4*>(qs + c * 8192 + r * 128 + ((cu ^ (r & 7)) << 4))
+                   : make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl.bar_qfree);  // (release: the reads above are done)
 #pragma unroll
       for (int c0 = 0; c0 < D / 4; c0 += 16) {
         uint32_t w16[16];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const uint4 v = qpre[c0 / 4 + u];
+          const uint4 v = qv[c0 / 4 + u];
           w16[4 * u] = v.x;
           w16[4 * u + 1] = v.y;
           w16[4 * u + 2] = v.z;
@@ -451,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_q[g]);
+      if (threadIdx.x == 128) A64_STAMP(4, 4090, 2);  // (trace) chain 0 quarter 0: Q in TMEM
     }
     const int n = n_own[g];
     // own blocks ascend and end at j <= i: only the last can be the diagonal block
@@ -551,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- epilogue: the row sum of both halves, this half of the O columns
     l += __shfl_xor_sync(0xffffffffu, l, 16);
     mbar_wait(&bar_ofull[g], 0);
+    if (threadIdx.x == 128) A64_STAMP(4, 4090, 3);  // (trace) O complete
     tc_fence_after();
     const bool write = en && l > 0.f;
     const float inv_l = 1.f / l;
@@ -575,9 +610,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (write && a.lse && half == 0)
       a.lse[(long long)(gr.b * a.H + hg) * a.L + (long long)ig * kBS + r] = (m_used + __log2f(l)) * 0.69314718055994531f;
   }
+  if (threadIdx.x == 128) A64_STAMP(4, 4090, 4);  // (trace) chain 0 quarter 0: epilogue stored
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 32) A64_STAMP(4, 4090, 5);  // (trace) TMEM released: exit
 }
 
 // Selected key blocks j <= i of every mask row (one warp per row, lanes over the row's
@@ -646,7 +683,8 @@ __global__ void __launch_bounds__(1024) attn64_items_kernel(AttnArgs a) {
 }
 
 template <int D>
-us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st) {
+us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                       cudaStream_t st) {
   static_assert(A64Smem<D>::bytes(attn::kMaxW) <= 227 * 1024, "attn64_kernel shared memory");
   const int smem = A64Smem<D>::bytes(a.W);
   static std::atomic<uint64_t> attr_done{0};  // (the attribute: the largest W)
@@ -665,7 +703,7 @@ us_status launch_a64_t(const AttnArgs& a, const CUtensorMap& tmK, const CUtensor
     US_LAUNCH_CHECK("attn64_items_kernel");
     items = (long long)a.B * a.H_kv * ((a.H / a.H_kv * a.N + 3) / 4);
   }
-  attn64_kernel<D><<<unsigned(items), kThreads, smem, st>>>(tmK, tmV, a);
+  attn64_kernel<D><<<unsigned(items), kThreads, smem, st>>>(tmQ, tmK, tmV, a);
   US_LAUNCH_CHECK("attn64_kernel");
   return US_OK;
 }
@@ -680,13 +718,14 @@ size_t attention64_ws_bytes(int B, int H, int H_kv, int N) {
   return 4 * size_t(attention64_item_entries(B, H, H_kv, N)) + 8 * size_t(B) * H_kv + 4 * size_t(B) * H * N;
 }
 
-us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st) {
+us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                             cudaStream_t st) {
   if (a.N > kMaxN) {
     set_error("attention: N (=L/S) above 4096 is not supported on the GPU path");
     return US_ERR_UNSUPPORTED;
   }
-  if (a.D == 128) return launch_a64_t<128>(a, tmK, tmV, st);
-  if (a.D == 64) return launch_a64_t<64>(a, tmK, tmV, st);
+  if (a.D == 128) return launch_a64_t<128>(a, tmQ, tmK, tmV, st);
+  if (a.D == 64) return launch_a64_t<64>(a, tmQ, tmK, tmV, st);
   set_error("attention: d_k must be 64 or 128 on the GPU path");
   return US_ERR_UNSUPPORTED;
 }

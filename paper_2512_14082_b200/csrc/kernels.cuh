@@ -166,7 +166,8 @@ us_status launch_attention_tp(const AttnArgs& a, const CUtensorMap& tmQ, const C
 // One M = 64 UMMA chain per query group (attention64.cu): same work decomposition and
 // union list as launch_attention, two groups per set of TMEM columns at lane offsets 0 / 16.
 // tmK / tmV: 3-D rows-chunked maps (box 64 rows).
-us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmK, const CUtensorMap& tmV, cudaStream_t st);
+us_status launch_attention64(const AttnArgs& a, const CUtensorMap& tmQ, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                             cudaStream_t st);
 // int32 entries of the attention64 work-item table (a.items) for these dims, and the bytes
 // of its workspace region: [item table][sel_pairs: B * H_kv u64][row_counts: B * H * N int32]
 long long attention64_item_entries(int B, int H, int H_kv, int N);
