@@ -352,7 +352,8 @@ def test_automatic_choice_follows_the_density_gate(density, H, H_kv, d):
             assert torch.equal(out[0][1][b, hs], out[want][1][b, hs]), (b, g, frac, want)
 
 
-@pytest.mark.parametrize("N,H,H_kv,d", [(33, 8, 2, 128), (45, 6, 6, 64), (45, 7, 1, 128)])
+@pytest.mark.parametrize("N,H,H_kv,d", [(33, 8, 2, 128), (45, 6, 6, 64), (45, 7, 1, 128), (1, 4, 1, 128),
+                                          (2, 8, 2, 64)])
 def test_attention64_odd_block_counts(N, H, H_kv, d):
     """attention64.cu (forced, and through the automatic gate) at block counts that end
     mid-word of the 32-bit mask rows, with GQA, MHA and G = 7 (a CTA's four chains drawn
