@@ -703,7 +703,7 @@ def main():
     # MUFU floor: ex2 at 16 results / clock / SM (B300_MICROARCH, measured here by
     # tools/ex2_rate.py) at the sustained clock; the proxy exponentiates every logit of the
     # full square (softmax_aggregation / 4 exps, metrics.cpp:62), the attention kernel 7/8 of
-    # its issued P entries (1/8 go to the FMA-pipe polynomial)
+    # its issued P entries (attention.cu sends 1/8 to the FMA-pipe polynomial)
     mufu_per_s = 16 * 148 * (clk["sm_mhz"] or 1965.0) * 1e6
     n_exp_proxy = (L // cq) * (L // ck) * (len(heads) // ch) * len(shard.batch)
     stage_roofs["proxy"] = {"bound": "tensor", "flops": qk,
@@ -712,7 +712,8 @@ def main():
                             "mufu_floor_ms": n_exp_proxy / mufu_per_s * 1e3}
     if issued_attn:
         useful_exp = selected * 64 * 64
-        stage_roofs["attention"]["mufu_floor_ms"] = useful_exp * 7 / 8 / mufu_per_s * 1e3
+        # (attention64.cu runs every exponential on the MUFU, attention.cu 7/8 of them)
+        stage_roofs["attention"]["mufu_floor_ms"] = useful_exp * (1.0 if m64 else 7 / 8) / mufu_per_s * 1e3
         stage_roofs["attention"]["tensor_floor_ms_issued"] = (issued_attn / (tf_sust * 1e12)) * 1e3
 
     if rank != 0:

@@ -107,7 +107,13 @@ struct A64Smem {
 
 constexpr uint32_t kTS = 0, kTO = 64, kTQ = 192;
 constexpr int kThreads = 24 * 32;
-constexpr int kPolyFrom = 28;  // columns >= this of each 32-column half of an off-diagonal block: FMA-pipe exp2
+// columns >= this of each 32-column half of an off-diagonal block: FMA-pipe exp2. 32 = none:
+// at C3 the polynomial share only costs (28: +0.5 / +1.3 %, 24: +1.5 / +2.3 %, 16: +4 / +5.5 %
+// at gain 9 / 8, profiles/r02d) — the FMA pipe, not the MUFU, is the contended one here
+#ifndef US_A64_POLY_FROM
+#define US_A64_POLY_FROM 32
+#endif
+constexpr int kPolyFrom = US_A64_POLY_FROM;
 
 __device__ __forceinline__ int issuer_group(int warp) { return warp == 20 ? 3 : warp - 1; }
 
