@@ -332,6 +332,23 @@ constexpr int kFusedWarps = kFusedThreads / 32;
 constexpr int kFusedMaxW = kFbMaxN / 32;
 constexpr int kRadixBins = 256;
 constexpr int kMaxFacTiles = 256;  // c = 8 fast path: key tiles per row (L/8/128 <= 256 at L <= 256K)
+// calibration knobs (tools/build_src_variant.sh): scores per thread in flight in the score
+// phase, resident CTAs per SM asked of ptxas, warp-aggregated histogram updates
+#ifndef US_SEL_INFLIGHT
+#define US_SEL_INFLIGHT 4
+#endif
+#ifndef US_SEL_MINB
+#define US_SEL_MINB 1
+#endif
+#ifndef US_SEL_AGG
+#define US_SEL_AGG 0
+#endif
+#ifndef US_SEL_GRID_PER_SM
+#define US_SEL_GRID_PER_SM 16
+#endif
+#ifndef US_SEL_PREFETCH
+#define US_SEL_PREFETCH 1
+#endif
 
 __device__ __forceinline__ double block_sum_f64(double v, double* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -376,7 +393,7 @@ __device__ __forceinline__ void word_scan(const int* cnt, int* pre, int W) {
 
 // Dynamic shared memory: the row's scores (N floats) then the radix histogram.
 template <int SW, int RQ, int SPB>
-__global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const ProxyArgs pa, const SelectArgs sa) {
+__global__ void __launch_bounds__(kFusedThreads, US_SEL_MINB) select_fused_kernel(const ProxyArgs pa, const SelectArgs sa) {
   extern __shared__ __align__(16) uint8_t fsm[];
   float* sc = reinterpret_cast<float*>(fsm);
   uint32_t* hist = reinterpret_cast<uint32_t*>(fsm + size_t(sa.N) * 4);
@@ -413,16 +430,16 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
     bool bad = false, nonfinite = false;
     // four scores per thread in flight (their partial loads issued together);
     // indices past the row are clamped for the loads and discarded
-    for (int j0 = tid; j0 < n; j0 += 4 * kFusedThreads) {
-      float fv[4];
+    for (int j0 = tid; j0 < n; j0 += US_SEL_INFLIGHT * kFusedThreads) {
+      float fv[US_SEL_INFLIGHT];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < US_SEL_INFLIGHT; ++u) {
         const int jj = min(j0 + u * kFusedThreads, n - 1);
         if constexpr (kFac) fv[u] = proxy_block_score_fac<SW, (RQ > 0 ? RQ : 1), (SPB > 0 ? SPB : 1)>(pa, plane, i, jj, fac_sh);
         else fv[u] = proxy_block_score<SW, RQ, SPB>(pa, plane, i, jj, lse_sh);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < US_SEL_INFLIGHT; ++u) {
         const int j = j0 + u * kFusedThreads;
         if (j < n) {
           float f = fv[u];
@@ -440,7 +457,7 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
     }
     // prefetch the partials of this CTA's NEXT row into L2 while this row is selected
     // (rows are read once from DRAM; the selection phases issue no loads)
-    {
+    if (US_SEL_PREFETCH) {
       const long long rn = rr + gridDim.x;
       if (rn < sa.rows) {
         const int plane2 = int(rn % planes), i2 = N - 1 - int(rn / planes);
@@ -494,10 +511,25 @@ __global__ void __launch_bounds__(kFusedThreads) select_fused_kernel(const Proxy
         hist[tid] = 0u;
         hist[tid + kFusedThreads] = 0u;
         __syncthreads();
+#if US_SEL_AGG
+        // one shared-memory atomic per distinct bin per warp (integer sums: the
+        // histogram is the same in any order)
+        for (int jb = tid - lane; jb < n; jb += kFusedThreads) {
+          const int j = jb + lane;
+          const uint32_t x = j < n ? __float_as_uint(sc[j]) : 0u;
+          const bool in = j < n && (x & pmask) == prefix;
+          const uint32_t bin = in ? (x >> sh) & dmask : 0xFFFFFFFFu;
+          const uint32_t v = in ? (topk ? 1u : uint32_t(__uint_as_float(x) * fscale_f)) : 0u;
+          const unsigned peers = __match_any_sync(0xffffffffu, bin);
+          const uint32_t sum = __reduce_add_sync(peers, v);
+          if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], sum);
+        }
+#else
         for (int j = tid; j < n; j += kFusedThreads) {
           const uint32_t x = __float_as_uint(sc[j]);
           if ((x & pmask) == prefix) atomicAdd(&hist[(x >> sh) & dmask], topk ? 1u : uint32_t(sc[j] * fscale_f));
         }
+#endif
         __syncthreads();
         // exclusive suffix over threads of their two bins: warp suffix scan, then the warps above
         const uint32_t h0 = hist[2 * tid], h1 = hist[2 * tid + 1];
@@ -756,7 +788,7 @@ void launch_fused_t(const ProxyArgs& pa, const SelectArgs& sa, cudaStream_t st) 
   // scores + bins + the per-(tile, row) factors of the c = 8 path: <= 25 KB (no attribute needed)
   const int smem = sa.N * 4 + kRadixBins * 4 + (RQ > 0 && SPB > 0 ? kMaxFacTiles * RQ * 4 : 0);
   long long blocks = sa.rows;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * US_SEL_GRID_PER_SM) blocks = 148 * US_SEL_GRID_PER_SM;
   select_fused_kernel<SW, RQ, SPB><<<unsigned(blocks), kFusedThreads, smem, st>>>(pa, sa);
   if (sa.select_mode == US_SELECT_TOP_P) select_fallback_fused_kernel<SW, RQ, SPB><<<148, 256, 0, st>>>(pa, sa);
 }
