@@ -46,6 +46,14 @@ constexpr int kRows = 128;  // composite query rows per CTA (UMMA M)
 constexpr int kKeys = kProxyKeys;  // composite keys per tile (UMMA N)
 // TMEM columns: S buffers [0,128) and [128,256); Q hi at 256, Q lo at 320 (D/2 cols each).
 constexpr uint32_t kTS0 = 0, kTQh = 256, kTQl = 320;
+// K-tile producer warps: one TMA-issuing warp sustains only ~20-29 B/clk of copies
+// (profiles/r02d/tma_probe.txt) while the fp16x3 MMAs consume a 64 KB hi+lo tile per
+// ~1700-2000 cycles (33-38 B/clk); with 2, warp 10 issues the second d-chunk of every tile.
+#ifndef US_PROXY_KPROD
+#define US_PROXY_KPROD 1
+#endif
+constexpr int kKProd = US_PROXY_KPROD;
+constexpr int kProxyThreads = (10 + (kKProd - 1)) * 32;
 
 template <int D>
 struct ProxySmem {
@@ -63,7 +71,7 @@ __device__ __forceinline__ int live_keys(int t, int c_q, int c_k, int Lk, int mo
 }
 
 template <int D, int SW, bool X3>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kProxyThreads, 1)
     proxy_kernel(const __grid_constant__ CUtensorMap tmKh, const __grid_constant__ CUtensorMap tmKl,
                  const ProxyArgs a) {
   using L = ProxySmem<D>;
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(320, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 8);
     for (int s = 0; s < kST; ++s) {
-      mbar_init(&bar_kfull[s], 1);
+      mbar_init(&bar_kfull[s], X3 && D == 128 ? kKProd : 1);
       mbar_init(&bar_kempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -109,9 +117,12 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
+  if (warp == 0 || warp >= 10) {
+    // ------------------------------------------------------------ TMA producer(s)
+    // (kKProd = 2 with X3 and D = 128: warp 0 loads d-chunk 0 of hi and lo, warp 10 chunk 1)
+    const int pi = warp == 0 ? 0 : 1;
+    const int np = X3 && D == 128 ? kKProd : 1;
+    if (pi < np && elect_one()) {
       tma_prefetch_desc(&tmKh);
       tma_prefetch_desc(&tmKl);
       const uint64_t pol = policy_evict_last();  // K tiles are re-read by every row tile
@@ -122,8 +133,8 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* kl = kh + L::kKBytes;
         const int krow = kplane * a.Lk + t * kKeys;
         if (X3) {
-          mbar_arrive_expect_tx(&bar_kfull[s], 2 * L::kKBytes);
-          for (int kc = 0; kc < L::kChunks; ++kc) {
+          mbar_arrive_expect_tx(&bar_kfull[s], 2 * L::kKBytes / np);
+          for (int kc = pi; kc < L::kChunks; kc += np) {
             tma_load_2d_hint(kh + kc * kKeys * 128, &tmKh, &bar_kfull[s], kc * 64, krow, pol);
             tma_load_2d_hint(kl + kc * kKeys * 128, &tmKl, &bar_kfull[s], kc * 64, krow, pol);
           }
@@ -336,7 +347,7 @@ us_status launch_proxy_x(const ProxyArgs& a, const CUtensorMap& tmKh, const CUte
   static std::atomic<uint64_t> attr_done{0};
   if (us_status s = ensure_smem_attr(kern, smem, attr_done, "proxy_kernel smem attribute"); s != US_OK) return s;
   dim3 grid((a.Lq + kRows - 1) / kRows, a.Hc, a.B);
-  kern<<<grid, 320, smem, st>>>(tmKh, tmKl, a);
+  kern<<<grid, kProxyThreads, smem, st>>>(tmKh, tmKl, a);
   US_LAUNCH_CHECK("proxy_kernel");
   if (!a.finalize) return US_OK;
   const dim3 fgrid(a.N, a.B * a.Hc);
