@@ -91,6 +91,13 @@ class NvmlClockSampler:
             self.stop_ev.wait(0.01)
 
     def start(self):
+        # one untimed query of each kind first: the first NVML calls of a process can take
+        # longer than a whole timed region (one r02 box returned a single sample)
+        try:
+            self.n.nvmlDeviceGetClockInfo(self.h, self.n.NVML_CLOCK_SM)
+            self.n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:  # noqa: BLE001 - sampling is best effort
+            pass
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
 
