@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
         // for it); the issuers learn which loads exist from kv_issued
         for (int x = 0; x < NT; ++x)
           if (((ls.steps[t] >> (12 + 2 * x)) & 3u) == 0u) mbar_arrive(&bar_kvempty[s]);
-        *reinterpret_cast<volatile int*>(&kv_issued) = t + 1;
+        st_release_cta(&kv_issued, t + 1);
 #endif
       }
     }
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(NT == 2 ? 384 : 192, NT == 2 ? 1 : 2)
       // wait on kvfull(tt) only once the producer has ISSUED load tt, which implies load
       // tt - kST landed (its release needed it) — the barrier is at most one phase behind,
       // and it cannot be ahead (this tile still holds tt).
-      while (*reinterpret_cast<const volatile int*>(&kv_issued) <= tt) __nanosleep(20);
+      while (ld_acquire_cta(&kv_issued) <= tt) __nanosleep(20);
 #endif
       mbar_wait(&bar_kvfull[tt % kST], (tt / kST) & 1);
       if (lane == 0) TRACE(x, kk, 8);  // K/V of the step has landed

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (u % np != me) continue;  // another producer's load of this sequence
         const int s = u % nst;
-        while (*reinterpret_cast<const volatile int*>(issued) < u) {
+        while (ld_acquire_cta(issued) < u) {
         }
         // (load u - nst armed => load u - 2 nst released: the parity wait is within one phase)
         if (u >= nst) mbar_wait(&empty[s], ((u / nst) + 1) & 1);
@@ -359,8 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 4; ++c)
             if ((mrow[c * a.W + wj] & bj) == 0u) mbar_arrive(&empty[s]);
         }
-        __threadfence_block();
-        *reinterpret_cast<volatile int*>(issued) = u + 1;
+        st_release_cta(issued, u + 1);
         tma_load_3d_hint(ring + s * SL::kKVBytes, tm, &full[s], 0, kvrow0 + j * kBS, 0, pol_kv);
         A64_STAMP(4, u, is_v ? 1 : 0);  // (trace) K / V load u issued
       }
@@ -379,11 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // load u - kKS has landed (its release needed it); the barrier cannot be ahead (this
     // chain holds u).
     auto wait_k = [&](int u) {
-      while (*reinterpret_cast<const volatile int*>(&k_issued) <= u) __nanosleep(20);
+      while (ld_acquire_cta(&k_issued) <= u) __nanosleep(20);
       mbar_wait(&bar_kfull[u % kKS], (u / kKS) & 1);
     };
     auto wait_v = [&](int u) {
-      while (*reinterpret_cast<const volatile int*>(&v_issued) <= u) __nanosleep(20);
+      while (ld_acquire_cta(&v_issued) <= u) __nanosleep(20);
       mbar_wait(&bar_vfull[u % kVS], (u / kVS) & 1);
     };
     auto issue_s = [&](int kk, int u) {
@@ -421,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // position before u, which every chain releases without waiting on this one.
       mbar_wait(&bar_sfree[g], k & 1);
       const bool early =
-          u1 >= 0 && ((kUnion && u1 - u < kKS) || (*reinterpret_cast<const volatile int*>(&k_issued) > u1 &&
+          u1 >= 0 && ((kUnion && u1 - u < kKS) || (ld_acquire_cta(&k_issued) > u1 &&
                                                    mbar_test_wait(&bar_kfull[u1 % kKS], (u1 / kKS) & 1)));
       if (early) issue_s(k + 1, u1);
       mbar_wait(&bar_pfull[g], k & 1);  // P(k) of the group's 64 rows is in SMEM

@@ -14,6 +14,20 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Inter-warp counters in shared memory (CTA scope): a release store publishes every
+// earlier write of the thread (e.g. an armed mbarrier); an acquire load orders the
+// reader's later accesses after it (the PTX memory model's defined alternative to a
+// volatile flag behind __threadfence_block; racecheck still lists these accesses as
+// hazards because it does not model acquire / release, profiles/r02k).
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
