@@ -69,6 +69,9 @@ __device__ int g_a64_trace_cta = -1;
 #endif
 // load order: 1 = union (ascending j over the four chains' blocks, a block two chains
 // selected loaded once), 0 = step-major (round k: the k-th block of each chain)
+#ifndef US_A64_QBY_ISSUER  // 1: group g's MMA issuer warp issues its Q copy at CTA start
+#define US_A64_QBY_ISSUER 1  //    (0: the four producers, after the union count, ahead of K / V;
+#endif                       //    1 is 40 us faster at 1-32 blocks per row, profiles/r02k)
 #ifndef US_A64_UNION
 #define US_A64_UNION 1
 #endif
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // idle until the first V loads: four producers issue them at once (one issuing warp's
       // copies proceed one at a time), fully coalesced — the softmax warps' own 16-B row
       // loads of Q took ~7 k cycles at CTA start and held the first K copy behind them
-      {
+      if (!US_A64_QBY_ISSUER) {
         const int gq = pw;
         if (gr.en[gq]) {
           mbar_arrive_expect_tx(&ctl.bar_qfull[gq], SL::kKVBytes);
@@ -404,6 +407,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
+    if (US_A64_QBY_ISSUER) {
+      // group g's 64 Q rows (16 KB at d = 128) into V stage g; this warp is idle until they
+      // are in TMEM, and the producers' first copies are then K / V only
+      if (elect_one()) {
+        if (gr.en[g]) {
+          mbar_arrive_expect_tx(&ctl.bar_qfull[g], SL::kKVBytes);
+          tma_load_3d_hint(smem + (kKS + g) * SL::kKVBytes, &tmQ, &ctl.bar_qfull[g], 0,
+                           (gr.b * a.H + gr.h[g]) * a.L + gr.i[g] * kBS, 0, policy_evict_first());
+        } else {
+          mbar_arrive(&ctl.bar_qfull[g]);
+        }
+      }
+      __syncwarp();
+    }
     mbar_wait(&bar_q[g], 0);  // Q rows of group g are in TMEM
     tc_fence_after();
     OwnWalk ow = own_start(g);
