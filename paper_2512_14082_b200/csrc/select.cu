@@ -347,11 +347,14 @@ constexpr int kMaxFacTiles = 256;  // c = 8 fast path: key tiles per row (L/8/12
 #ifndef US_SEL_AGG
 #define US_SEL_AGG 0
 #endif
+// grid 32 x 148 CTAs without the L2 prefetch of each CTA's next row: -4.5 % at C3 vs
+// 16 x 148 with it (profiles/r02k; the 9 resident CTAs per SM already keep enough loads
+// in flight, and the prefetched rows of 2 x 1332 CTAs overflow the L2)
 #ifndef US_SEL_GRID_PER_SM
-#define US_SEL_GRID_PER_SM 16
+#define US_SEL_GRID_PER_SM 32
 #endif
 #ifndef US_SEL_PREFETCH
-#define US_SEL_PREFETCH 1
+#define US_SEL_PREFETCH 0
 #endif
 
 __device__ __forceinline__ double block_sum_f64(double v, double* sh) {
