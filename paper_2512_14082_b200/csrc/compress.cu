@@ -85,7 +85,10 @@ __device__ __forceinline__ double group_sum(double v, int width) {
 // F32: f32 input storage (the reference's own HeadStack<float>, C1): every strategy
 // sums in fp64 in row order like the oracle; the bf16 fp32-exact fast path is skipped.
 template <int STRAT, bool F32>
-__global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? 3 : 1) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
+#ifndef US_COMPRESS_MINB  // resident 256-thread CTAs asked of ptxas for the mean kernel
+#define US_COMPRESS_MINB 3
+#endif
+__global__ void __launch_bounds__(256, STRAT == US_POOL_MEAN ? US_COMPRESS_MINB : 1) compress_kernel(CompressArgs a, double inv_c, double inv_m) {
   const int chunks = a.d / 8;
   const int Lc = a.L / a.c;
   const long long total = (long long)a.B * a.planes * Lc * chunks;
