@@ -49,6 +49,9 @@ constexpr uint32_t kTS0 = 0, kTQh = 256, kTQl = 320;
 // K-tile producer warps: one TMA-issuing warp sustains only ~20-29 B/clk of copies
 // (profiles/r02d/tma_probe.txt) while the fp16x3 MMAs consume a 64 KB hi+lo tile per
 // ~1700-2000 cycles (33-38 B/clk); with 2, warp 10 issues the second d-chunk of every tile.
+#ifndef US_PROXY_FMA  // 1: exponent arguments as one FFMA2 of the raw logits (see the epilogue)
+#define US_PROXY_FMA 1
+#endif
 #ifndef US_PROXY_KPROD
 #define US_PROXY_KPROD 1
 #endif
@@ -249,6 +252,19 @@ __global__ void __launch_bounds__(kProxyThreads, 1)
       float m8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) m8[u] = -INFINITY;
+#if US_PROXY_FMA
+      // max over the raw logits, scaled once (k2 > 0: RN scaling is monotonic, so this is
+      // the max of the scaled logits bit for bit); the exponent argument below is then one
+      // FFMA2 (x k2 - mt, a single rounding) instead of a multiply and an add
+#pragma unroll
+      for (int c = 0; c < kKeys; ++c) {
+        x[c] = c < nvalid ? __uint_as_float(v[c]) : -INFINITY;
+        m8[c & 7] = fmaxf(m8[c & 7], x[c]);
+      }
+      const float mraw = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      const float mt = mraw == -INFINITY ? -INFINITY : mraw * k2;
+#else
 #pragma unroll
       for (int c = 0; c < kKeys; ++c) {
         x[c] = c < nvalid ? __uint_as_float(v[c]) * k2 : -INFINITY;
@@ -256,6 +272,7 @@ __global__ void __launch_bounds__(kProxyThreads, 1)
       }
       const float mt = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                              fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+#endif
       // slot sums (fixed pairwise order inside each slot of SW keys)
       float slot[NS];
       if (mt == -INFINITY) {
@@ -263,9 +280,16 @@ __global__ void __launch_bounds__(kProxyThreads, 1)
         for (int s = 0; s < NS; ++s) slot[s] = 0.f;
       } else {
         const float2 nm = make_float2(-mt, -mt);
+#if US_PROXY_FMA
+        const float2 kk = make_float2(k2, k2);
+#endif
 #pragma unroll
         for (int c = 0; c < kKeys; c += 2) {
+#if US_PROXY_FMA
+          const float2 d2 = __ffma2_rn(make_float2(x[c], x[c + 1]), kk, nm);
+#else
           const float2 d2 = __fadd2_rn(make_float2(x[c], x[c + 1]), nm);
+#endif
           x[c] = ex2_approx(d2.x);
           x[c + 1] = ex2_approx(d2.y);
         }
