@@ -52,6 +52,9 @@ constexpr uint32_t kTS0 = 0, kTQh = 256, kTQl = 320;
 #ifndef US_PROXY_FMA  // 1: exponent arguments as one FFMA2 of the raw logits (see the epilogue)
 #define US_PROXY_FMA 1
 #endif
+#ifndef US_PROXY_FADD2  // 1: the slot sums' additions paired into FADD2 (same operands, same order)
+#define US_PROXY_FADD2 0
+#endif
 #ifndef US_PROXY_KPROD
 #define US_PROXY_KPROD 1
 #endif
@@ -293,10 +296,22 @@ __global__ void __launch_bounds__(kProxyThreads, 1)
           x[c] = ex2_approx(d2.x);
           x[c + 1] = ex2_approx(d2.y);
         }
+#if US_PROXY_FADD2
+        // the same additions, two per FADD2 (x[c] += x[c + w] and x[c + 2w] += x[c + 3w])
+#pragma unroll
+        for (int w = 1; w < SW; w <<= 1)
+#pragma unroll
+          for (int c = 0; c < kKeys; c += 4 * w) {
+            const float2 r = __fadd2_rn(make_float2(x[c], x[c + 2 * w]), make_float2(x[c + w], x[c + 3 * w]));
+            x[c] = r.x;
+            x[c + 2 * w] = r.y;
+          }
+#else
 #pragma unroll
         for (int w = 1; w < SW; w <<= 1)
 #pragma unroll
           for (int c = 0; c < kKeys; c += 2 * w) x[c] += x[c + w];
+#endif
 #pragma unroll
         for (int s = 0; s < NS; ++s) slot[s] = x[s * SW];
       }
