@@ -55,6 +55,9 @@ constexpr uint32_t kTS0 = 0, kTQh = 256, kTQl = 320;
 #ifndef US_PROXY_FADD2  // 1: the slot sums' additions paired into FADD2 (same operands, same order)
 #define US_PROXY_FADD2 0
 #endif
+#ifndef US_PROXY_FULLTILE  // 1: tiles whose keys are all live skip the per-key live test
+#define US_PROXY_FULLTILE 1
+#endif
 #ifndef US_PROXY_KPROD
 #define US_PROXY_KPROD 1
 #endif
@@ -259,10 +262,21 @@ __global__ void __launch_bounds__(kProxyThreads, 1)
       // max over the raw logits, scaled once (k2 > 0: RN scaling is monotonic, so this is
       // the max of the scaled logits bit for bit); the exponent argument below is then one
       // FFMA2 (x k2 - mt, a single rounding) instead of a multiply and an add
+#if US_PROXY_FULLTILE
+      if (nvalid >= kKeys) {  // every key of the tile live (all but the last tile of a row)
 #pragma unroll
-      for (int c = 0; c < kKeys; ++c) {
-        x[c] = c < nvalid ? __uint_as_float(v[c]) : -INFINITY;
-        m8[c & 7] = fmaxf(m8[c & 7], x[c]);
+        for (int c = 0; c < kKeys; ++c) {
+          x[c] = __uint_as_float(v[c]);
+          m8[c & 7] = fmaxf(m8[c & 7], x[c]);
+        }
+      } else
+#endif
+      {
+#pragma unroll
+        for (int c = 0; c < kKeys; ++c) {
+          x[c] = c < nvalid ? __uint_as_float(v[c]) : -INFINITY;
+          m8[c & 7] = fmaxf(m8[c & 7], x[c]);
+        }
       }
       const float mraw = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
